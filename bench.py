@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the TileLink B200 TP-MLP layer (BASELINE.json metric: TP-MLP layer TFLOPS & ms,
+vs non-overlapped NCCL + cuBLAS, % of roofline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1 : the LLaMA-7B MLP layer (M=8192 tokens, H=4096, I=11008, gated SiLU) on one B200, W = 1
+        (AG and RS degenerate to identities), through tl_mlp_forward's two kernels.
+        Also reports the same layer with W = 8 ranks emulated on the one GPU ("loopback_w8":
+        one launch drives all 8 ranks, so the full AG push / flag / RS push / owner-reduce
+        protocol runs, with peer stores landing in local HBM).
+N > 1 : one process per GPU under torchrun, tensor parallel W = N over NVLink (strong scaling:
+        the layer is fixed, M = 8192), IPC symmetric workspace bootstrapped over NCCL.
+--impl reference : the fp64 CPU oracle (oracle/tl_oracle.py) timed on the host cores on a
+        bounded row sample of the same workload (rank 0 only).
+One JSON line is printed by rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M_TOK, HID, FFN = 8192, 4096, 11008
+METRIC = "TP-MLP layer TFLOPS (LLaMA-7B MLP, gated SiLU)"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def layer_flops(M, H, I, W, gated=True):
+    """Algorithmic FLOPs per rank: GEMM1 2*M*H*N1 + GEMM2 2*M*(I/W)*H (activation negligible)."""
+    il = I // W
+    return 2 * M * H * (2 * il if gated else il), 2 * M * il * H
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            d = json.load(f)
+        return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    except Exception:
+        return 1590.0, 1400.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks sampler
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [s for s in sm if mx and s > 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm (oracle)
+def run_reference(args):
+    import numpy as np
+    import tl_inputs as TI
+    from oracle import tl_oracle as O
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    W = max(1, args.gpus)
+    X, G, U, W2 = TI.mlp_full(M_TOK, HID, FFN, seed=0)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    f = lambda L: [TI.to_f64(t) for t in L]
+    Xs, W1s, W2s = f(Xs), f(W1s), f(W2s)
+    rows_per_step = args.ref_rows
+    rng = np.random.default_rng(0)
+    g1, g2 = layer_flops(M_TOK, HID, FFN, W)
+    flops_per_row = (g1 + g2) * W / M_TOK     # whole-layer FLOPs per token (all ranks)
+    for _ in range(args.warmup):
+        O.mlp_forward_rows(Xs, W1s, W2s, TI.ACT_SILU_MUL, rng.choice(M_TOK, rows_per_step, replace=False))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.mlp_forward_rows(Xs, W1s, W2s, TI.ACT_SILU_MUL, rng.choice(M_TOK, rows_per_step, replace=False))
+    dt = time.perf_counter() - t0
+    tflops = flops_per_row * rows_per_step * args.steps / dt / 1e12
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(tflops, 6), "unit": "TFLOPS", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"llama7b_mlp_w{W}", "M": M_TOK, "H": HID, "I": FFN, "world": W, "act": "silu_mul",
+                   "sample_rows_per_step": rows_per_step},
+        "cpu_baseline": {"value": round(tflops, 6), "unit": "TFLOPS", "cores": cores, "kind": "oracle",
+                         "sample": f"{rows_per_step} random token rows of the M={M_TOK} layer per step (rows are "
+                                   f"independent, so the row-sampled oracle is exact for them); fp64 numpy"},
+        "e2e": {"value": round(tflops, 6), "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_leg(Xs_cpu, W1s_cpu, W2s_cpu, seconds):
+    """The oracle as it stands, timed on this host on a bounded row sample (~`seconds`)."""
+    import numpy as np
+    import tl_inputs as TI
+    from oracle import tl_oracle as O
+    f = lambda L: [TI.to_f64(t) for t in L]
+    Xs, W1s, W2s = f(Xs_cpu), f(W1s_cpu), f(W2s_cpu)
+    W = len(Xs)
+    g1, g2 = layer_flops(M_TOK, HID, FFN, W)
+    flops_per_row = (g1 + g2) * W / M_TOK
+    rng = np.random.default_rng(1)
+    rows = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        O.mlp_forward_rows(Xs, W1s, W2s, TI.ACT_SILU_MUL, rng.choice(M_TOK, 128, replace=False))
+        rows += 128
+    dt = time.perf_counter() - t0
+    return {"value": round(flops_per_row * rows / dt / 1e12, 6), "unit": "TFLOPS", "cores": os.cpu_count(),
+            "kind": "oracle", "sample": f"{rows} token rows of the M={M_TOK} layer (row-sampled fp64 oracle, "
+                                        f"{dt:.1f} s)"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-rows", type=int, default=64)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-loopback", action="store_true")
+    ap.add_argument("--no-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2503_20313_b200 as tl
+    import tl_inputs as TI
+    from paper_2503_20313_b200.bootstrap import max_over_ranks
+
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    distributed = world_env > 1
+    if distributed:
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        rank, W = dist.get_rank(), dist.get_world_size()
+    else:
+        torch.cuda.set_device(0)
+        rank, W = 0, 1
+    dev = torch.cuda.current_device()
+    P_burst, P_sust, peak_src = peaks()
+
+    # ---- inputs: full problem generated once (seeded), this rank's shards resident in HBM
+    X, G, U, W2 = TI.mlp_full(M_TOK, HID, FFN, seed=0)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    Mr, Il = M_TOK // W, FFN // W
+    x = Xs[rank].cuda()
+    w1 = W1s[rank].cuda()
+    w2 = W2s[rank].cuda()
+    out = torch.empty(Mr, HID, device="cuda", dtype=torch.bfloat16)
+    Z = torch.empty(M_TOK, Il, device="cuda", dtype=torch.bfloat16)
+    comm = tl.Comm.from_process_group(None, dev, M_TOK, HID) if distributed else tl.Comm.single(dev, M_TOK, HID)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        comm.ag_gemm(x, w1, Z, act=tl.ACT_SILU_MUL, stream=stream)   # kernel 1: AG + GEMM1 + SiLU*up
+        comm.gemm_rs(Z, w2, out, stream=stream)                     # kernel 2: GEMM2 + RS
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---- timed region: K steps, per-kernel CUDA events on the launching stream
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clocks = Clocks(dev)
+    clocks.start()
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        comm.ag_gemm(x, w1, Z, act=tl.ACT_SILU_MUL, stream=stream)
+        ev[i][1].record(stream)
+        comm.gemm_rs(Z, w2, out, stream=stream)
+        ev[i][2].record(stream)
+    t_end.record(stream)
+    barrier()
+    clk = clocks.stop()
+    total_ms = max_over_ranks(t_start.elapsed_time(t_end))
+    k1 = [e[0].elapsed_time(e[1]) for e in ev]
+    k2 = [e[1].elapsed_time(e[2]) for e in ev]
+    k1_ms = max_over_ranks(sum(k1) / len(k1))
+    k2_ms = max_over_ranks(sum(k2) / len(k2))
+    ms = total_ms / args.steps
+    st, diag = comm.check()
+    f1, f2 = layer_flops(M_TOK, HID, FFN, W)
+    value = (f1 + f2) * W / (ms * 1e-3) / 1e12        # whole job (all ranks), TFLOPS
+    per_gpu = value / W
+    ach1 = f1 / (k1_ms * 1e-3) / 1e12
+
+    # ---- parity spot-check of this run's output against the fp64 oracle (sampled rows)
+    parity = None
+    if rank == 0:
+        from oracle import tl_oracle as O
+        rows = list(range(0, Mr, max(1, Mr // 32)))[:32]
+        f = lambda L: [TI.to_f64(t) for t in L]
+        ref = O.mlp_forward_rows(f(Xs), f(W1s), f(W2s), TI.ACT_SILU_MUL, rows)
+        got = out.float().cpu().double().numpy()
+        parity = {"rows": len(rows), "rel_fro": O.rel_frobenius(np.stack([got[i] for i in rows]),
+                                                                np.stack([ref[i] for i in rows])),
+                  "tol": 5e-3, "status": int(st)}
+
+    # ---- end to end through the public API: pinned host X in, host out back, every step
+    x_host = Xs[rank].pin_memory()
+    out_host = torch.empty(Mr, HID, dtype=torch.bfloat16).pin_memory()
+    xin = torch.empty_like(x)
+
+    def e2e_step():
+        xin.copy_(x_host, non_blocking=True)
+        comm.mlp_forward(xin, w1, w2, out, act=tl.ACT_SILU_MUL, Z=Z, stream=stream)
+        out_host.copy_(out, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    e2e_val = (f1 + f2) * W / (e2e_ms * 1e-3) / 1e12
+
+    # ---- non-overlapped NCCL + cuBLAS baseline (same inputs, same protocol)
+    base = None
+    if not args.no_baseline:
+        xg = torch.empty(M_TOK, HID, device="cuda", dtype=torch.bfloat16)
+        part = torch.empty(M_TOK, HID, device="cuda", dtype=torch.bfloat16)
+        ob = torch.empty(Mr, HID, device="cuda", dtype=torch.bfloat16)
+
+        def base_step():
+            if distributed:
+                dist.all_gather_into_tensor(xg, x)
+                src = xg
+            else:
+                src = x
+            y = src @ w1.T
+            z = torch.nn.functional.silu(y[:, :Il]) * y[:, Il:]
+            if distributed:
+                torch.matmul(z, w2.T, out=part)
+                dist.reduce_scatter_tensor(ob, part)
+            else:
+                torch.matmul(z, w2.T, out=ob)
+
+        for _ in range(args.warmup):
+            base_step()
+        barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.steps):
+            base_step()
+        b1.record(stream)
+        barrier()
+        bms = max_over_ranks(b0.elapsed_time(b1)) / args.steps
+        base = {"impl": "nccl+cublas non-overlapped (torch.matmul, silu*mul, all_gather/reduce_scatter)",
+                "ms_per_step": round(bms, 4), "value": round((f1 + f2) * W / (bms * 1e-3) / 1e12, 2),
+                "unit": "TFLOPS", "speedup_ours": round(bms / ms, 4)}
+
+    # ---- W = 8 ranks emulated on this GPU (full fused protocol, one launch per kernel)
+    loop = None
+    if not distributed and not args.no_loopback:
+        LW = 8
+        Xs8, W1s8, W2s8 = TI.shard_mlp(X, G, U, W2, LW, TI.ACT_SILU_MUL)
+        lc = tl.Comm.loopback(LW, dev, M_TOK, HID)
+        xs8 = [t.cuda() for t in Xs8]
+        w18 = [t.cuda() for t in W1s8]
+        w28 = [t.cuda() for t in W2s8]
+        o8 = [torch.empty(M_TOK // LW, HID, device="cuda", dtype=torch.bfloat16) for _ in range(LW)]
+        z8 = [torch.empty(M_TOK, FFN // LW, device="cuda", dtype=torch.bfloat16) for _ in range(LW)]
+        for _ in range(args.warmup):
+            lc.ag_gemm_lb(xs8, w18, z8, act=tl.ACT_SILU_MUL)
+            lc.gemm_rs_lb(z8, w28, o8)
+        torch.cuda.synchronize()
+        le = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        for i in range(args.steps):
+            le[i][0].record(stream)
+            lc.ag_gemm_lb(xs8, w18, z8, act=tl.ACT_SILU_MUL)
+            le[i][1].record(stream)
+            lc.gemm_rs_lb(z8, w28, o8)
+            le[i][2].record(stream)
+        torch.cuda.synchronize()
+        lst, ldiag = lc.check()
+        l1 = sum(e[0].elapsed_time(e[1]) for e in le) / args.steps
+        l2 = sum(e[1].elapsed_time(e[2]) for e in le) / args.steps
+        from oracle import tl_oracle as O
+        rows = [0, 1000, 2047, 3000, 5000, 8191]
+        f = lambda L: [TI.to_f64(t) for t in L]
+        ref = O.mlp_forward_rows(f(Xs8), f(W1s8), f(W2s8), TI.ACT_SILU_MUL, rows)
+        mr8 = M_TOK // LW
+        got = np.stack([o8[i // mr8][i % mr8].float().cpu().double().numpy() for i in rows])
+        loop = {"world": LW, "mode": "loopback (8 ranks on 1 GPU, 18 CTAs each; peer stores -> local HBM)",
+                "ag_gemm_ms": round(l1, 4), "gemm_rs_ms": round(l2, 4), "ms_per_step": round(l1 + l2, 4),
+                "value": round((f1 + f2) / (l1 + l2) / 1e9, 2), "unit": "TFLOPS (whole layer, 1 GPU)",
+                "status": int(lst), "parity_rel_fro": O.rel_frobenius(got, np.stack([ref[i] for i in rows]))}
+        lc.close()
+
+    if rank != 0:
+        return
+    cpu = cpu_baseline_leg(Xs, W1s, W2s, args.cpu_seconds) if W == 1 else None
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "TFLOPS", "n_gpus": W, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"llama7b_mlp_w{W}", "M": M_TOK, "H": HID, "I": FFN, "world": W, "act": "silu_mul",
+                   "gemm1": f"[{M_TOK}x{HID}] x [{2 * Il}x{HID}]^T", "gemm2": f"[{M_TOK}x{Il}] x [{HID}x{Il}]^T",
+                   "parallelism": f"tp{W}", "l2": "inputs larger than L2 (W1 180 MB + W2 90 MB + X 64 MB > 126 MB)",
+                   "cta_pair": comm.get_option("cta_pair")},
+        "tflops_per_gpu": round(per_gpu, 2),
+        "kernels_ms": {"ag_gemm_silu": round(k1_ms, 4), "gemm_rs": round(k2_ms, 4)},
+        "roofline": {"bound": "tensor", "kernel": "tl_gemm_kernel (AG-GEMM1 + SiLU*up)", "achieved": round(ach1, 2),
+                     "peak": P_burst, "unit": "TFLOP/s", "frac": round(ach1 / P_burst, 4),
+                     "frac_sustained": round(ach1 / P_sust, 4), "peak_source": peak_src,
+                     "layer_frac": round(per_gpu / P_burst, 4), "traffic": None,
+                     "per_launch_flop": f1},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_val, 2), "unit": "TFLOPS", "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": out.numel() * 2,
+                "api": "tl_mlp_forward via paper_2503_20313_b200.Comm.mlp_forward, pinned host X in / out back"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk,
+        "parity": parity,
+        "baseline_nccl_cublas": base,
+        "loopback_w8": loop,
+    }
+    traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_path):
+        try:
+            line["roofline"]["traffic"] = json.load(open(traffic_path)).get("ag_gemm_silu_bytes")
+        except Exception:
+            pass
+    print(json.dumps(line), flush=True)
+    comm.close()
+    if distributed:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,179 @@
+/*
+ * tl_api.h -- C ABI of the B200-native TileLink tensor-parallel MLP hot path.
+ *
+ * What the library computes (arXiv 2503.20313, PAPER.md):
+ *   P:56  (Sec. 2.1) tensor-parallel FFN: "input data is gathered from different ranks,
+ *         followed by local computation using the corresponding weight shards. Finally,
+ *         the partial results are reduced and scattered to the appropriate ranks" --
+ *         AllGather + GEMM followed by GEMM + ReduceScatter.
+ *   P:607 (Sec. 7.2) "one activation layer (e.g., SiLUMul or GeLUMul) between these two parts".
+ *   P:236-271 (Table "Tile-centric primitives") the producer/consumer and peer signals and the
+ *         push data primitive that order communication tiles against compute tiles;
+ *   P:410-420 (Sec. 4.1) the static tile -> (shape, rank, channel) mapping.
+ *
+ * Everything runs in this library's sm_100a kernels (tcgen05/TMEM GEMM fed by TMA, in-kernel
+ * NVLink peer stores, per-tile epoch flags with acquire/release semantics).  There is no CPU
+ * fallback: every entry point that computes returns TL_ERR_CUDA when no usable device exists.
+ *
+ * Conventions for every op below
+ *   - Data: bf16 (uint16 storage), row-major, contiguous, 16-byte aligned device pointers.
+ *     Weights use the nn.Linear layout [out_features, in_features] (K contiguous).
+ *   - Accumulation fp32 in TMEM; outputs rounded once to bf16 (round-to-nearest-even).
+ *   - Collectives: with world > 1 every rank must call the same op with the same shapes in the
+ *     same order (SPMD).  All ops are asynchronous on `stream` (a cudaStream_t; NULL =
+ *     legacy default stream); the caller keeps every buffer alive until the stream passes.
+ *   - Ownership: the caller owns every pointer argument.  The comm owns its symmetric
+ *     workspace (gather buffers, reduce-scatter staging, flags, diagnostics) and, when the
+ *     caller passes Z_ws = NULL to tl_mlp_forward, a lazily grown local Z buffer.
+ *   - Errors: argument validation is synchronous and returns TL_ERR_INVALID / TL_ERR_UNSUPPORTED
+ *     before anything is launched (nothing is written).  A launch failure returns TL_ERR_CUDA.
+ *     A device-side wait that exceeds the timeout (option "timeout_ms") does not hang: the kernel
+ *     records {rank, kind, index, observed, expected, epoch} and finishes; tl_comm_check then
+ *     returns TL_ERR_TIMEOUT.  No C++ exception crosses the ABI.  tl_last_error() gives a
+ *     human-readable message for the last failure on the calling thread.
+ *   - Threads: one host thread per comm.
+ */
+#ifndef TL_API_H
+#define TL_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef struct tl_comm* tl_comm_t;
+
+typedef enum {
+  TL_OK = 0,
+  TL_ERR_INVALID = 1,      /* bad argument (null/misaligned pointer, shape mismatch, over capacity) */
+  TL_ERR_UNSUPPORTED = 2,  /* valid request this build does not implement (e.g. M/W % 128 != 0 for RS) */
+  TL_ERR_CUDA = 3,         /* CUDA runtime/driver failure or no sm_100 device */
+  TL_ERR_TIMEOUT = 4,      /* a device-side flag wait exceeded timeout_ms (see tl_comm_check) */
+  TL_ERR_STATE = 5         /* comm used before connect / after destroy */
+} tl_status;
+
+/* Activation between the two GEMMs. For the *_MUL acts GEMM1's weight is the stacked
+ * [gate_r; up_r] of shape [2*I_local, H] and Z = act(X.gate_r^T) * (X.up_r^T), [M, I_local]. */
+typedef enum { TL_ACT_NONE = 0, TL_ACT_SILU_MUL = 1, TL_ACT_GELU_TANH_MUL = 2 } tl_act;
+
+const char* tl_status_string(tl_status s);
+const char* tl_last_error(void);
+const char* tl_build_info(void);       /* compile target + version string */
+
+/* ---------------------------------------------------------------- comm lifecycle ----------
+ * Symmetric workspace replacing the paper's NVSHMEM heap: one device allocation per
+ * rank holding 2 banks of the gathered activation X_full [max_M, max_H] and 2 banks of the
+ * reduce-scatter staging [world][max_M/world, max_H], plus per-tile u32 flags and a diag
+ * block.  Banks alternate by call parity; flags hold monotone epoch values (never reset).
+ *
+ * Multi-process (one process per GPU):
+ *   tl_comm_create(rank, world, device, caps, my_handle, &c)   -- allocates, zeroes flags,
+ *       writes tl_handle_size() bytes of IPC handle into my_handle (caller memory);
+ *   the caller all-gathers the handles (e.g. torch.distributed, rank order) -- this exchange
+ *       is the only synchronisation needed before connect;
+ *   tl_comm_connect(c, all_handles) -- all_handles = world * tl_handle_size() bytes in rank
+ *       order; opens the peers' workspaces (cudaIpcOpenMemHandle).
+ * Single-process loopback (all `world` ranks emulated on ONE device, one launch drives all
+ * ranks concurrently, peers are local buffers; used by the single-GPU tests and benches):
+ *   tl_comm_create_loopback(world, device, caps, &c)  -- ready to use, no connect.
+ * Capacities: max_M = largest global M, max_H = largest AG width K (= H) and RS width N (= H). */
+size_t tl_handle_size(void);
+tl_status tl_comm_create(int rank, int world, int device, int64_t max_M, int64_t max_H,
+                         void* my_handle, tl_comm_t* out);
+tl_status tl_comm_connect(tl_comm_t comm, const void* all_handles);
+tl_status tl_comm_create_loopback(int world, int device, int64_t max_M, int64_t max_H,
+                                  tl_comm_t* out);
+tl_status tl_comm_destroy(tl_comm_t comm);
+/* rank (-1 for loopback), world, number of ranks driven by this process (1 or world). */
+tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
+
+/* Options (the decoupled design space), each also settable by env TL_<KEY upper>:
+ *   "comm_tile_rows"   Tm_p, rows per AG producer tile (default 64; 16..M/world)
+ *   "channels_per_rank" C, barrier channels per rank (default 0 = one per producer tile);
+ *                      a consumer tile waits on every producer tile of every channel its rows
+ *                      span (P:410-420, P:313 trade-off)
+ *   "copy_ctas"        CTAs per rank that run the AG copy role (default 0 = all)
+ *   "rs_order"         0 = one-shot push to owner slots + fp32 owner reduce, 1 = ring (Fig. gemm_rs)
+ *   "cta_pair"         2 = tcgen05 cta_group::2 (256-row tiles on an SM pair), 1 = single SM
+ *   "raster_group"     m-blocks per rasterisation group (default 8)
+ *   "num_ctas"         CTAs per rank (default: all SMs / local ranks, rounded to the pair size)
+ *   "timeout_ms"       device-side flag-wait timeout (default 10000)
+ *   "debug_drop_notify" (fault injection) index g >= 0 of one AG producer-tile notify to skip
+ *                      on rank "debug_drop_rank" (default -1 = off); the waiting rank reports
+ *                      TL_ERR_TIMEOUT instead of hanging
+ *   "debug_drop_rank"  see above */
+tl_status tl_set_option(tl_comm_t comm, const char* key, int64_t value);
+tl_status tl_get_option(tl_comm_t comm, const char* key, int64_t* value);
+
+/* Synchronises the device, then returns TL_OK or TL_ERR_TIMEOUT and fills
+ * diag_out[0..7] = {status, rank, kind (1 = AG wait, 2 = RS wait), src rank, index,
+ * observed, expected, epoch} of the first timed-out wait (zeros if none).  Clears the record. */
+tl_status tl_comm_check(tl_comm_t comm, int64_t diag_out[8]);
+
+/* ---------------------------------------------------------------- the three ops -----------
+ * AG-GEMM (P:56 first half):
+ *   C[M, N_local] = AllGather_rows(A_shard)[M, K] . B^T
+ *   A_shard bf16 [M/world, K] (rows r*M/world.. of the global A), B bf16 [N_local, K],
+ *   C bf16 [M, N_local], A_gathered nullable bf16 [M, K] (receives the gathered A; debug).
+ *   Constraints: M % world == 0, K % 8 == 0, N_local % 8 == 0, M <= max_M, K <= max_H.
+ * tl_ag_gemm_act: same with the fused activation epilogue: B = [gate; up] of [2*N_out, K] and
+ *   C = act(A.gate^T) * (A.up^T) of [M, N_out] (N_out % 8 == 0).  act = NONE == tl_ag_gemm. */
+tl_status tl_ag_gemm(tl_comm_t comm, const void* A_shard, const void* B, void* C,
+                     void* A_gathered, int64_t M, int64_t N_local, int64_t K, void* stream);
+tl_status tl_ag_gemm_act(tl_comm_t comm, const void* A_shard, const void* B, void* C,
+                         void* A_gathered, int64_t M, int64_t N_out, int64_t K, tl_act act,
+                         void* stream);
+
+/* GEMM-RS (P:56 second half):
+ *   C_shard[M/world, N] = rows [r*M/world, (r+1)*M/world) of sum_{s} A_s . B_s^T
+ *   A bf16 [M, K_local], B bf16 [N, K_local], C_shard bf16 [M/world, N].
+ *   Constraints: M % world == 0, K_local % 8 == 0, N % 8 == 0, N <= max_H, M <= max_M, and for
+ *   world > 1 (M/world) % 128 == 0 (owner rows per 128-row CTA tile). */
+tl_status tl_gemm_rs(tl_comm_t comm, const void* A, const void* B, void* C_shard,
+                     int64_t M, int64_t N, int64_t K_local, void* stream);
+
+/* MLP forward (P:56 + P:607): out_shard = RS( act( AG(X_shard) . W1^T ) . W2^T )
+ *   X_shard bf16 [M/world, H]; W1 bf16 [N1, H] with N1 = I_local (NONE) or 2*I_local
+ *   ([gate_r; up_r], *_MUL); W2 bf16 [H, I_local]; out_shard bf16 [M/world, H];
+ *   Z_ws nullable bf16 [M, I_local] (receives Z when given).  Both kernels are stream-ordered
+ *   on `stream`, with no host synchronisation between them. */
+tl_status tl_mlp_forward(tl_comm_t comm, const void* X_shard, const void* W1, const void* W2,
+                         void* out_shard, void* Z_ws, int64_t M, int64_t H, int64_t I_local,
+                         tl_act act, void* stream);
+
+/* ---------------------------------------------------------------- loopback variants -------
+ * Same operations for a loopback comm: every pointer argument becomes an array of `world`
+ * pointers, entry r being rank r's buffer (all on the comm's device).  One kernel launch
+ * runs all ranks concurrently (each rank on its own CTAs), so the flag protocol is exercised
+ * exactly as across GPUs, with peer stores landing in local memory. */
+tl_status tl_ag_gemm_loopback(tl_comm_t comm, const void* const* A_shard, const void* const* B,
+                              void* const* C, void* const* A_gathered, int64_t M,
+                              int64_t N_out, int64_t K, tl_act act, void* stream);
+tl_status tl_gemm_rs_loopback(tl_comm_t comm, const void* const* A, const void* const* B,
+                              void* const* C_shard, int64_t M, int64_t N, int64_t K_local,
+                              void* stream);
+tl_status tl_mlp_forward_loopback(tl_comm_t comm, const void* const* X_shard,
+                                  const void* const* W1, const void* const* W2,
+                                  void* const* out_shard, void* const* Z_ws, int64_t M,
+                                  int64_t H, int64_t I_local, tl_act act, void* stream);
+
+/* ---------------------------------------------------------------- diagnostics -------------
+ * Evaluates the device-side static mapping for producer tiles t = 0..n-1 of a
+ * gathered M-row tensor on `world` ranks with Tm_p rows per tile and C channels per rank, in a
+ * kernel, and copies {row_lo, row_hi, src_rank, channel} per tile to host memory out[4*n].
+ * Used by the bit-exact index tests. */
+tl_status tl_debug_static_map(int64_t M, int world, int64_t tm_rows, int channels_per_rank,
+                              int64_t n, int64_t* out);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* TL_API_H */

@@ -1,0 +1,172 @@
+"""B200-native TileLink tensor-parallel MLP hot path (arXiv 2503.20313).
+
+Thin Python binding over the C ABI in include/tl_api.h.  PyTorch is used only for device
+memory, streams and process groups; every step of AG-GEMM / GEMM-RS / MLP runs in the
+library's sm_100a kernels.  There is no CPU fallback: without the built library or an sm_100
+device every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from ._lib import TLError, check, lib, ptr_array
+
+ACT_NONE, ACT_SILU_MUL, ACT_GELU_TANH_MUL = 0, 1, 2
+ACTS = {"none": ACT_NONE, "silu_mul": ACT_SILU_MUL, "gelu_tanh_mul": ACT_GELU_TANH_MUL}
+
+__all__ = ["Comm", "TLError", "lib", "ACT_NONE", "ACT_SILU_MUL", "ACT_GELU_TANH_MUL", "static_map_device"]
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _bf16(t, name):
+    import torch
+    if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor")
+    return t
+
+
+class Comm:
+    """A TileLink communicator: symmetric workspace + epochs (tl_comm_t)."""
+
+    def __init__(self, handle, rank, world, local_ranks, device):
+        self._h = C.c_void_p(handle)
+        self.rank, self.world, self.local_ranks, self.device = rank, world, local_ranks, device
+
+    # ------------------------------------------------------------------ construction
+    @classmethod
+    def loopback(cls, world: int, device: int = 0, max_M: int = 8192, max_H: int = 4096):
+        """All `world` ranks emulated on one device, driven by single launches."""
+        L = lib()
+        h = C.c_void_p()
+        check(L.tl_comm_create_loopback(world, device, max_M, max_H, C.byref(h)), "tl_comm_create_loopback")
+        return cls(h.value, -1, world, world, device)
+
+    @classmethod
+    def single(cls, device: int = 0, max_M: int = 8192, max_H: int = 4096):
+        """World of one rank (AG/RS degenerate to identities)."""
+        L = lib()
+        h = C.c_void_p()
+        buf = C.create_string_buffer(L.tl_handle_size())
+        check(L.tl_comm_create(0, 1, device, max_M, max_H, buf, C.byref(h)), "tl_comm_create")
+        return cls(h.value, 0, 1, 1, device)
+
+    @classmethod
+    def from_process_group(cls, group=None, device: int | None = None, max_M: int = 8192, max_H: int = 4096):
+        """One process per GPU: create, all-gather the IPC handles over `group`, connect."""
+        import torch
+        import torch.distributed as dist
+        from .bootstrap import exchange_handles
+        L = lib()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if device is None:
+            device = torch.cuda.current_device()
+        h = C.c_void_p()
+        buf = C.create_string_buffer(L.tl_handle_size())
+        check(L.tl_comm_create(rank, world, device, max_M, max_H, buf, C.byref(h)), "tl_comm_create")
+        comm = cls(h.value, rank, world, 1, device)
+        if world > 1:
+            allh = exchange_handles(bytes(buf.raw), group)
+            check(L.tl_comm_connect(comm._h, C.create_string_buffer(allh, len(allh))), "tl_comm_connect")
+            dist.barrier(group)
+        return comm
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().tl_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ options / diag
+    def set_option(self, key: str, value: int):
+        check(lib().tl_set_option(self._h, key.encode(), int(value)), "tl_set_option")
+
+    def get_option(self, key: str) -> int:
+        v = C.c_int64()
+        check(lib().tl_get_option(self._h, key.encode(), C.byref(v)), "tl_get_option")
+        return v.value
+
+    def check(self):
+        """(status, diag[8]) after synchronising the device (tl_comm_check)."""
+        d = (C.c_int64 * 8)()
+        st = lib().tl_comm_check(self._h, d)
+        return st, list(d)
+
+    # ------------------------------------------------------------------ ops (one rank per process)
+    def ag_gemm(self, A_shard, B, C_out, A_gathered=None, act: int = ACT_NONE, stream=None):
+        M = A_shard.shape[0] * self.world
+        K = A_shard.shape[1]
+        N = C_out.shape[1]
+        check(lib().tl_ag_gemm_act(self._h, _ptr(A_shard), _ptr(B), _ptr(C_out), _ptr(A_gathered), M, N, K, act,
+                                   _stream(stream)), "tl_ag_gemm_act")
+        return C_out
+
+    def gemm_rs(self, A, B, C_shard, stream=None):
+        M, K = A.shape
+        N = B.shape[0]
+        check(lib().tl_gemm_rs(self._h, _ptr(A), _ptr(B), _ptr(C_shard), M, N, K, _stream(stream)), "tl_gemm_rs")
+        return C_shard
+
+    def mlp_forward(self, X_shard, W1, W2, out_shard, act: int = ACT_SILU_MUL, Z=None, stream=None):
+        M = X_shard.shape[0] * self.world
+        H = X_shard.shape[1]
+        I_l = W2.shape[1]
+        check(lib().tl_mlp_forward(self._h, _ptr(X_shard), _ptr(W1), _ptr(W2), _ptr(out_shard), _ptr(Z), M, H, I_l,
+                                   act, _stream(stream)), "tl_mlp_forward")
+        return out_shard
+
+    # ------------------------------------------------------------------ ops (loopback: lists per rank)
+    def ag_gemm_lb(self, A_shards, Bs, Cs, A_gathered=None, act: int = ACT_NONE, stream=None):
+        W = self.world
+        M = A_shards[0].shape[0] * W
+        K = A_shards[0].shape[1]
+        N = Cs[0].shape[1]
+        a, _ka = ptr_array([_ptr(t) for t in A_shards])
+        b, _kb = ptr_array([_ptr(t) for t in Bs])
+        c, _kc = ptr_array([_ptr(t) for t in Cs])
+        g, _kg = ptr_array([_ptr(t) for t in A_gathered]) if A_gathered is not None else (None, None)
+        check(lib().tl_ag_gemm_loopback(self._h, a, b, c, g, M, N, K, act, _stream(stream)), "tl_ag_gemm_loopback")
+        return Cs
+
+    def gemm_rs_lb(self, As, Bs, Cs, stream=None):
+        M, K = As[0].shape
+        N = Bs[0].shape[0]
+        a, _ka = ptr_array([_ptr(t) for t in As])
+        b, _kb = ptr_array([_ptr(t) for t in Bs])
+        c, _kc = ptr_array([_ptr(t) for t in Cs])
+        check(lib().tl_gemm_rs_loopback(self._h, a, b, c, M, N, K, _stream(stream)), "tl_gemm_rs_loopback")
+        return Cs
+
+    def mlp_forward_lb(self, X_shards, W1s, W2s, outs, act: int = ACT_SILU_MUL, Zs=None, stream=None):
+        W = self.world
+        M = X_shards[0].shape[0] * W
+        H = X_shards[0].shape[1]
+        I_l = W2s[0].shape[1]
+        x, _kx = ptr_array([_ptr(t) for t in X_shards])
+        w1, _k1 = ptr_array([_ptr(t) for t in W1s])
+        w2, _k2 = ptr_array([_ptr(t) for t in W2s])
+        o, _ko = ptr_array([_ptr(t) for t in outs])
+        z, _kz = ptr_array([_ptr(t) for t in Zs]) if Zs is not None else (None, None)
+        check(lib().tl_mlp_forward_loopback(self._h, x, w1, w2, o, z, M, H, I_l, act, _stream(stream)),
+              "tl_mlp_forward_loopback")
+        return outs
+
+
+def static_map_device(M: int, world: int, tm_rows: int, channels_per_rank: int, n: int):
+    """Device-evaluated static mapping rows (row_lo, row_hi, src_rank, channel) for tiles 0..n-1."""
+    out = (C.c_int64 * (4 * n))()
+    check(lib().tl_debug_static_map(M, world, tm_rows, channels_per_rank, n, out), "tl_debug_static_map")
+    return [tuple(out[4 * i:4 * i + 4]) for i in range(n)]

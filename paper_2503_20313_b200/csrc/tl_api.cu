@@ -1,0 +1,732 @@
+// tl_api.cu -- host side of the C ABI declared in include/tl_api.h: symmetric workspace
+// (CUDA IPC, replacing the paper's NVSHMEM runtime), epochs/banks,
+// argument validation, TMA descriptor construction and kernel launches.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cctype>
+#include <cstdarg>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+
+#include "../../include/tl_api.h"
+#include "tl_kernel.cuh"
+#include "tl_params.h"
+
+using namespace tl;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+tl_status fail(tl_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+#define TL_CUDA(call)                                                                             \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return fail(TL_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr uint32_t kMagic = 0x544C4232u;  // "TLB2"
+constexpr size_t kAlign = 1 << 20;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Handle {
+  uint32_t magic, version;
+  int32_t rank, world;
+  int64_t max_M, max_H;
+  uint64_t ws_bytes;
+  cudaIpcMemHandle_t ipc;
+};
+
+// Workspace layout of one rank (identical on every rank: symmetric).
+struct WsLayout {
+  size_t xfull[2], stage[2], ag_flags, rs_flags, diag, bytes;
+  static WsLayout make(int world, int64_t max_M, int64_t max_H) {
+    WsLayout l;
+    const size_t xb = align_up((size_t)max_M * max_H * 2, kAlign);
+    size_t off = 0;
+    for (int b = 0; b < 2; ++b) l.xfull[b] = off, off += xb;
+    for (int b = 0; b < 2; ++b) l.stage[b] = off, off += xb;   // [world][max_M/world][max_H]
+    l.ag_flags = off, off += align_up((size_t)world * kAgFlagStride * 4, kAlign);
+    l.rs_flags = off, off += align_up((size_t)world * kRsFlagStride * 4, kAlign);
+    l.diag = off, off += kAlign;
+    l.bytes = off;
+    return l;
+  }
+  size_t flags_begin() const { return ag_flags; }
+  size_t flags_bytes() const { return bytes - ag_flags; }
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+tl_status get_encode() {
+  if (g_encode) return TL_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || fn == nullptr || q != cudaDriverEntryPointSuccess)
+    return fail(TL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable: %s", cudaGetErrorString(e));
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return TL_OK;
+}
+
+// 2D bf16 row-major [rows, cols] (row pitch = cols), boxes of box_cols x box_rows, 128B swizzle.
+tl_status make_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                    uint32_t box_cols) {
+  tl_status s = get_encode();
+  if (s != TL_OK) return s;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TL_ERR_CUDA, "cuTensorMapEncodeTiled(rows=%llu cols=%llu box=%ux%u) failed: %d",
+                (unsigned long long)rows, (unsigned long long)cols, box_rows, box_cols, (int)r);
+  return TL_OK;
+}
+
+struct Options {
+  int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
+          raster_group = 8, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1;
+};
+
+struct OptDesc {
+  const char* key;
+  int64_t Options::*field;
+  int64_t lo, hi;
+};
+const OptDesc kOpts[] = {
+    {"comm_tile_rows", &Options::comm_tile_rows, 16, 1 << 20},
+    {"channels_per_rank", &Options::channels_per_rank, 0, 1 << 20},
+    {"copy_ctas", &Options::copy_ctas, 0, 4096},
+    {"rs_order", &Options::rs_order, 0, 1},
+    {"cta_pair", &Options::cta_pair, 1, 2},
+    {"raster_group", &Options::raster_group, 1, 1 << 20},
+    {"num_ctas", &Options::num_ctas, 0, 4096},
+    {"timeout_ms", &Options::timeout_ms, 1, 1ll << 40},
+    {"debug_drop_notify", &Options::debug_drop_notify, -1, 1 << 30},
+    {"debug_drop_rank", &Options::debug_drop_rank, -1, kMaxWorld - 1},
+};
+
+}  // namespace
+
+struct tl_comm {
+  int rank = -1, world = 1, n_local = 1, device = 0, sm_count = 148;
+  bool loopback = false, connected = false;
+  int64_t max_M = 0, max_H = 0;
+  WsLayout lay{};
+  uint8_t* ws[kMaxWorld] = {};      // workspace base of every rank (own, loopback-owned or IPC-mapped)
+  bool owned[kMaxWorld] = {};       // cudaMalloc'd by us (else IPC-opened)
+  uint32_t ag_epoch = 0, rs_epoch = 0;
+  Options opt;
+  void* z[kMaxWorld] = {};          // local Z workspaces (mlp_forward with Z_ws = NULL)
+  size_t z_bytes[kMaxWorld] = {};
+  std::map<std::tuple<const void*, uint64_t, uint64_t, uint32_t, uint32_t>, CUtensorMap> tmaps;
+};
+
+namespace {
+
+void apply_env(Options& o) {
+  for (const auto& d : kOpts) {
+    std::string env = "TL_";
+    for (const char* c = d.key; *c; ++c) env += (char)toupper(*c);
+    const char* v = getenv(env.c_str());
+    if (v && *v) {
+      long long x = atoll(v);
+      if (x >= d.lo && x <= d.hi) o.*(d.field) = x;
+    }
+  }
+}
+
+tl_status cached_tmap(tl_comm* c, CUtensorMap* out, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                      uint32_t box_cols) {
+  auto key = std::make_tuple(ptr, rows, cols, box_rows, box_cols);
+  auto it = c->tmaps.find(key);
+  if (it != c->tmaps.end()) {
+    *out = it->second;
+    return TL_OK;
+  }
+  tl_status s = make_tmap(out, ptr, rows, cols, box_rows, box_cols);
+  if (s != TL_OK) return s;
+  if (c->tmaps.size() > 4096) c->tmaps.clear();
+  c->tmaps.emplace(key, *out);
+  return TL_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+tl_status check_comm(tl_comm* c) {
+  if (!c) return fail(TL_ERR_INVALID, "null comm");
+  if (!c->connected) return fail(TL_ERR_STATE, "comm not connected");
+  return TL_OK;
+}
+
+int pair_of(const tl_comm* c) { return c->opt.cta_pair == 1 ? 1 : 2; }
+
+int ctas_per_rank(const tl_comm* c) {
+  const int pair = pair_of(c);
+  int n = c->opt.num_ctas > 0 ? (int)c->opt.num_ctas : c->sm_count / c->n_local;
+  if (n * c->n_local > c->sm_count) n = c->sm_count / c->n_local;
+  n = n / pair * pair;
+  return n < pair ? pair : n;
+}
+
+template <int kPair, int kEpi, bool kAG>
+tl_status launch_t(tl_comm* c, const Params& p, cudaStream_t stream) {
+  constexpr int kStages = stages_for(kPair, kAG);
+  using L = Layout<kPair, kStages, kAG>;
+  auto kern = tl_gemm_kernel<kPair, kStages, kEpi, kAG>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::smem_request));
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_local * p.ctas_per_rank);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = L::smem_request;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kPair;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TL_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+  return TL_OK;
+}
+
+tl_status launch(tl_comm* c, const Params& p, int epi, bool ag, cudaStream_t s) {
+  const int pair = pair_of(c);
+  if (pair == 2) {
+    if (epi == EPI_STORE) return ag ? launch_t<2, EPI_STORE, true>(c, p, s) : launch_t<2, EPI_STORE, false>(c, p, s);
+    if (epi == EPI_SILU_MUL)
+      return ag ? launch_t<2, EPI_SILU_MUL, true>(c, p, s) : launch_t<2, EPI_SILU_MUL, false>(c, p, s);
+    if (epi == EPI_GELU_MUL)
+      return ag ? launch_t<2, EPI_GELU_MUL, true>(c, p, s) : launch_t<2, EPI_GELU_MUL, false>(c, p, s);
+    return launch_t<2, EPI_RS, false>(c, p, s);
+  }
+  if (epi == EPI_STORE) return ag ? launch_t<1, EPI_STORE, true>(c, p, s) : launch_t<1, EPI_STORE, false>(c, p, s);
+  if (epi == EPI_SILU_MUL)
+    return ag ? launch_t<1, EPI_SILU_MUL, true>(c, p, s) : launch_t<1, EPI_SILU_MUL, false>(c, p, s);
+  if (epi == EPI_GELU_MUL)
+    return ag ? launch_t<1, EPI_GELU_MUL, true>(c, p, s) : launch_t<1, EPI_GELU_MUL, false>(c, p, s);
+  return launch_t<1, EPI_RS, false>(c, p, s);
+}
+
+tl_status zero_fill(void* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return TL_OK;
+  tl_zero_kernel<<<296, 256, 0, s>>>(reinterpret_cast<uint16_t*>(out), n);
+  TL_CUDA(cudaGetLastError());
+  return TL_OK;
+}
+
+int local_rank_id(const tl_comm* c, int i) { return c->loopback ? i : c->rank; }
+
+void fill_common(tl_comm* c, Params& p) {
+  memset(&p, 0, sizeof(p));
+  p.world = c->world;
+  p.n_local = c->n_local;
+  p.ctas_per_rank = ctas_per_rank(c);
+  p.raster_group = (int)c->opt.raster_group;
+  p.timeout_ns = (uint64_t)c->opt.timeout_ms * 1000000ull;
+  p.diag = reinterpret_cast<Diag*>(c->ws[c->loopback ? 0 : c->rank] + c->lay.diag);
+  p.drop_rank = (int)c->opt.debug_drop_rank;
+  p.drop_index = (int)c->opt.debug_drop_notify;
+}
+
+// ---------------------------------------------------------------- AG-GEMM (+ act)
+tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, void* const* C,
+                       void* const* Agath, int64_t M, int64_t N_out, int64_t K, int act, cudaStream_t stream) {
+  tl_status st = check_comm(c);
+  if (st != TL_OK) return st;
+  const int W = c->world;
+  if (M < 0 || N_out < 0 || K < 0) return fail(TL_ERR_INVALID, "negative dimension");
+  if (act < TL_ACT_NONE || act > TL_ACT_GELU_TANH_MUL) return fail(TL_ERR_INVALID, "bad act %d", act);
+  if (M % W) return fail(TL_ERR_INVALID, "M=%lld not divisible by world=%d", (long long)M, W);
+  if (K % 8 || N_out % 8) return fail(TL_ERR_INVALID, "K and N must be multiples of 8 (K=%lld N=%lld)",
+                                      (long long)K, (long long)N_out);
+  if (M > c->max_M || K > c->max_H)
+    return fail(TL_ERR_INVALID, "M=%lld K=%lld exceed comm capacity (%lld, %lld)", (long long)M, (long long)K,
+                (long long)c->max_M, (long long)c->max_H);
+  if (M >= (1ll << 31) || N_out >= (1ll << 31) || K >= (1ll << 31)) return fail(TL_ERR_UNSUPPORTED, "dimension >= 2^31");
+  for (int i = 0; i < c->n_local; ++i) {
+    if (!A[i] || !B[i] || !C[i]) return fail(TL_ERR_INVALID, "null pointer (rank slot %d)", i);
+    if (!aligned16(A[i]) || !aligned16(B[i]) || !aligned16(C[i]) || (Agath && Agath[i] && !aligned16(Agath[i])))
+      return fail(TL_ERR_INVALID, "pointers must be 16-byte aligned");
+  }
+  const int64_t M_r = M / W;
+  StaticMap sm = StaticMap::make((int)M, W, (int)std::max<int64_t>(1, std::min<int64_t>(c->opt.comm_tile_rows, M_r)),
+                                 (int)c->opt.channels_per_rank);
+  if (W > 1 && sm.tiles_per_rank > kAgFlagStride)
+    return fail(TL_ERR_UNSUPPORTED, "too many producer tiles per rank (%d > %d): raise comm_tile_rows",
+                sm.tiles_per_rank, kAgFlagStride);
+  if (M == 0 || N_out == 0) return TL_OK;
+  if (K == 0) {
+    for (int i = 0; i < c->n_local; ++i) {
+      st = zero_fill(C[i], M * N_out, stream);
+      if (st != TL_OK) return st;
+    }
+    return TL_OK;
+  }
+  TL_CUDA(cudaSetDevice(c->device));
+  const bool comm = W > 1;
+  const uint32_t epoch = comm ? ++c->ag_epoch : 0;
+  const int bank = epoch & 1;
+
+  Params* pp = new Params;  // ~6 KB: keep it off the stack
+  Params& p = *pp;
+  fill_common(c, p);
+  const int pair = pair_of(c);
+  p.M = (int)M;
+  p.N_out = (int)N_out;
+  p.K = (int)K;
+  p.M_r = (int)M_r;
+  p.epoch = epoch;
+  p.m_blocks = (int)((M + 128 * pair - 1) / (128 * pair));
+  p.n_blocks = (int)((N_out + (act ? 128 : 256) - 1) / (act ? 128 : 256));
+  p.k_blocks = (int)((K + kBK - 1) / kBK);
+  p.tm_rows = sm.Tm;
+  p.tiles_per_rank = sm.tiles_per_rank;
+  p.tiles_per_channel = sm.tiles_per_channel;
+  p.copy_ctas = c->opt.copy_ctas > 0 ? (int)std::min<int64_t>(c->opt.copy_ctas, p.ctas_per_rank) : p.ctas_per_rank;
+  p.row_bytes = (int)(K * 2);
+  p.rs_mode = RS_NONE;
+  if (comm) {
+    p.order = (M_r % (128 * pair) == 0) ? ORDER_AG_INTERLEAVE : ORDER_ROTATE;
+    for (int d = 0; d < W; ++d) {
+      p.xfull[d] = c->ws[d] + c->lay.xfull[bank];
+      p.ag_flags[d] = reinterpret_cast<uint32_t*>(c->ws[d] + c->lay.ag_flags);
+    }
+  } else {
+    p.order = ORDER_IDENTITY;
+  }
+  for (int i = 0; i < c->n_local; ++i) {
+    RankArgs& ra = p.rk[i];
+    const int r = local_rank_id(c, i);
+    ra.rank = r;
+    ra.a_shard = reinterpret_cast<const uint8_t*>(A[i]);
+    ra.m_rot = (int)((r * M_r) / (128 * pair));
+    const void* a_src = comm ? (const void*)(c->ws[r] + c->lay.xfull[bank]) : A[i];
+    if ((st = cached_tmap(c, &ra.tm_a, a_src, M, K, 128, 64)) != TL_OK) break;
+    if (act == TL_ACT_NONE) {
+      if ((st = cached_tmap(c, &ra.tm_b0, B[i], N_out, K, pair == 2 ? 128 : 256, 64)) != TL_OK) break;
+    } else {
+      if ((st = cached_tmap(c, &ra.tm_b0, B[i], N_out, K, 128, 64)) != TL_OK) break;
+      const void* up = reinterpret_cast<const uint8_t*>(B[i]) + (size_t)N_out * K * 2;
+      if (!aligned16(up)) { st = fail(TL_ERR_INVALID, "up half misaligned"); break; }
+      if ((st = cached_tmap(c, &ra.tm_b1, up, N_out, K, 128, 64)) != TL_OK) break;
+    }
+    if ((st = cached_tmap(c, &ra.tm_c, C[i], M, N_out, 32, 64)) != TL_OK) break;
+  }
+  if (st == TL_OK) {
+    const int epi = act == TL_ACT_NONE ? EPI_STORE : act == TL_ACT_SILU_MUL ? EPI_SILU_MUL : EPI_GELU_MUL;
+    st = launch(c, p, epi, comm, stream);
+  }
+  delete pp;
+  if (st != TL_OK) return st;
+  if (Agath) {
+    for (int i = 0; i < c->n_local; ++i) {
+      if (!Agath[i]) continue;
+      const int r = local_rank_id(c, i);
+      const void* src = comm ? (const void*)(c->ws[r] + c->lay.xfull[bank]) : A[i];
+      TL_CUDA(cudaMemcpyAsync(Agath[i], src, (size_t)M * K * 2, cudaMemcpyDeviceToDevice, stream));
+    }
+  }
+  return TL_OK;
+}
+
+// ---------------------------------------------------------------- GEMM-RS
+tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, void* const* C, int64_t M, int64_t N,
+                       int64_t K, cudaStream_t stream) {
+  tl_status st = check_comm(c);
+  if (st != TL_OK) return st;
+  const int W = c->world;
+  if (M < 0 || N < 0 || K < 0) return fail(TL_ERR_INVALID, "negative dimension");
+  if (M % W) return fail(TL_ERR_INVALID, "M=%lld not divisible by world=%d", (long long)M, W);
+  if (K % 8 || N % 8) return fail(TL_ERR_INVALID, "K and N must be multiples of 8 (K=%lld N=%lld)", (long long)K,
+                                  (long long)N);
+  if (M > c->max_M || N > c->max_H)
+    return fail(TL_ERR_INVALID, "M=%lld N=%lld exceed comm capacity (%lld, %lld)", (long long)M, (long long)N,
+                (long long)c->max_M, (long long)c->max_H);
+  if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31)) return fail(TL_ERR_UNSUPPORTED, "dimension >= 2^31");
+  const int64_t M_r = M / W;
+  const int pair = pair_of(c);
+  const int64_t n_blocks = (N + 255) / 256;
+  if (W > 1) {
+    if (M_r % 128) return fail(TL_ERR_UNSUPPORTED, "GEMM-RS with world > 1 needs (M/world) %% 128 == 0 (M/world=%lld)",
+                               (long long)M_r);
+    if ((M_r / 128) * n_blocks > kRsFlagStride) return fail(TL_ERR_UNSUPPORTED, "too many RS tiles per owner block");
+  }
+  for (int i = 0; i < c->n_local; ++i) {
+    if (!A[i] || !B[i] || !C[i]) return fail(TL_ERR_INVALID, "null pointer (rank slot %d)", i);
+    if (!aligned16(A[i]) || !aligned16(B[i]) || !aligned16(C[i])) return fail(TL_ERR_INVALID, "pointers must be 16-byte aligned");
+  }
+  if (M == 0 || N == 0) return TL_OK;
+  if (K == 0) {
+    for (int i = 0; i < c->n_local; ++i)
+      if ((st = zero_fill(C[i], M_r * N, stream)) != TL_OK) return st;
+    return TL_OK;
+  }
+  TL_CUDA(cudaSetDevice(c->device));
+  const bool comm = W > 1;
+  const uint32_t epoch = comm ? ++c->rs_epoch : 0;
+  const int bank = epoch & 1;
+  Params* pp = new Params;
+  Params& p = *pp;
+  fill_common(c, p);
+  p.M = (int)M;
+  p.N_out = (int)N;
+  p.K = (int)K;
+  p.M_r = (int)M_r;
+  p.epoch = epoch;
+  p.m_blocks = (int)((M + 128 * pair - 1) / (128 * pair));
+  p.n_blocks = (int)n_blocks;
+  p.k_blocks = (int)((K + kBK - 1) / kBK);
+  p.rs_mode = comm ? (c->opt.rs_order == 1 ? RS_RING : RS_ONESHOT) : RS_NONE;
+  p.order = comm ? ORDER_ROTATE : ORDER_IDENTITY;
+  p.tm_rows = 1;
+  p.tiles_per_rank = 1;
+  p.tiles_per_channel = 1;
+  if (comm) {
+    for (int o = 0; o < W; ++o) {
+      uint8_t* sb = c->ws[o] + c->lay.stage[bank];
+      p.staging[o] = reinterpret_cast<const uint16_t*>(sb);
+      p.rs_flags[o] = reinterpret_cast<uint32_t*>(c->ws[o] + c->lay.rs_flags);
+      if ((st = cached_tmap(c, &p.tm_stage[o], sb, (uint64_t)W * M_r, N, 32, 64)) != TL_OK) break;
+    }
+  }
+  for (int i = 0; st == TL_OK && i < c->n_local; ++i) {
+    RankArgs& ra = p.rk[i];
+    const int r = local_rank_id(c, i);
+    ra.rank = r;
+    // owner order r+1, ..., r+W-1, r: remote partials leave first, the own block is reduced last
+    ra.m_rot = comm ? (int)((((r + 1) % W) * M_r) / (128 * pair)) : 0;
+    if ((st = cached_tmap(c, &ra.tm_a, A[i], M, K, 128, 64)) != TL_OK) break;
+    if ((st = cached_tmap(c, &ra.tm_b0, B[i], N, K, pair == 2 ? 128 : 256, 64)) != TL_OK) break;
+    if ((st = cached_tmap(c, &ra.tm_c, C[i], comm ? M_r : M, N, 32, 64)) != TL_OK) break;
+  }
+  if (st == TL_OK) st = launch(c, p, comm ? EPI_RS : EPI_STORE, false, stream);
+  delete pp;
+  return st;
+}
+
+tl_status mlp_impl(tl_comm* c, const void* const* X, const void* const* W1, const void* const* W2, void* const* out,
+                   void* const* Zws, int64_t M, int64_t H, int64_t I_l, int act, cudaStream_t stream) {
+  tl_status st = check_comm(c);
+  if (st != TL_OK) return st;
+  if (M < 0 || H < 0 || I_l < 0) return fail(TL_ERR_INVALID, "negative dimension");
+  if (I_l % 8) return fail(TL_ERR_INVALID, "I_local must be a multiple of 8");
+  void* z[kMaxWorld];
+  for (int i = 0; i < c->n_local; ++i) {
+    if (Zws && Zws[i]) {
+      z[i] = Zws[i];
+      continue;
+    }
+    const size_t need = (size_t)std::max<int64_t>(M, 1) * std::max<int64_t>(I_l, 1) * 2;
+    if (c->z_bytes[i] < need) {
+      TL_CUDA(cudaSetDevice(c->device));
+      if (c->z[i]) {
+        TL_CUDA(cudaStreamSynchronize(stream));
+        TL_CUDA(cudaFree(c->z[i]));
+        c->z[i] = nullptr;
+        c->z_bytes[i] = 0;
+      }
+      TL_CUDA(cudaMalloc(&c->z[i], need));
+      c->z_bytes[i] = need;
+    }
+    z[i] = c->z[i];
+  }
+  // Validate the second half before launching the first (nothing is written on error).
+  if (c->world > 1 && (M / c->world) % 128)
+    return fail(TL_ERR_UNSUPPORTED, "MLP with world > 1 needs (M/world) %% 128 == 0");
+  if (H > c->max_H || M > c->max_M) return fail(TL_ERR_INVALID, "M/H exceed comm capacity");
+  for (int i = 0; i < c->n_local; ++i)
+    if (!out[i] || !aligned16(out[i]) || !W2[i] || !aligned16(W2[i])) return fail(TL_ERR_INVALID, "bad out/W2 pointer");
+  st = ag_gemm_impl(c, X, W1, z, nullptr, M, I_l, H, act, stream);
+  if (st != TL_OK) return st;
+  return gemm_rs_impl(c, z, W2, out, M, H, I_l, stream);
+}
+
+tl_status alloc_ws(tl_comm* c, int r) {
+  void* p = nullptr;
+  TL_CUDA(cudaMalloc(&p, c->lay.bytes));
+  c->ws[r] = reinterpret_cast<uint8_t*>(p);
+  c->owned[r] = true;
+  TL_CUDA(cudaMemset(c->ws[r] + c->lay.flags_begin(), 0, c->lay.flags_bytes()));
+  return TL_OK;
+}
+
+tl_status init_common(tl_comm* c, int world, int device, int64_t max_M, int64_t max_H) {
+  if (world < 1 || world > kMaxWorld) return fail(TL_ERR_UNSUPPORTED, "world must be in [1, %d]", kMaxWorld);
+  if (max_M < 1 || max_H < 8) return fail(TL_ERR_INVALID, "bad capacities");
+  int n = 0;
+  TL_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(TL_ERR_CUDA, "device %d not present (%d devices)", device, n);
+  cudaDeviceProp prop;
+  TL_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(TL_ERR_CUDA, "device %d is sm_%d%d; this build needs sm_100", device, prop.major, prop.minor);
+  TL_CUDA(cudaSetDevice(device));
+  c->world = world;
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  c->max_M = (max_M + world - 1) / world * world;
+  c->max_H = (max_H + 7) / 8 * 8;
+  c->lay = WsLayout::make(world, c->max_M, c->max_H);
+  apply_env(c->opt);
+  return TL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tl_status_string(tl_status s) {
+  switch (s) {
+    case TL_OK: return "TL_OK";
+    case TL_ERR_INVALID: return "TL_ERR_INVALID";
+    case TL_ERR_UNSUPPORTED: return "TL_ERR_UNSUPPORTED";
+    case TL_ERR_CUDA: return "TL_ERR_CUDA";
+    case TL_ERR_TIMEOUT: return "TL_ERR_TIMEOUT";
+    case TL_ERR_STATE: return "TL_ERR_STATE";
+  }
+  return "TL_ERR_UNKNOWN";
+}
+
+const char* tl_last_error(void) { return g_last_error.c_str(); }
+
+const char* tl_build_info(void) { return "tilelink-b200 sm_100a tcgen05/TMA build " __DATE__; }
+
+size_t tl_handle_size(void) { return sizeof(Handle); }
+
+tl_status tl_comm_create(int rank, int world, int device, int64_t max_M, int64_t max_H, void* my_handle,
+                         tl_comm_t* out) {
+  if (!out || !my_handle) return fail(TL_ERR_INVALID, "null out/my_handle");
+  *out = nullptr;
+  if (rank < 0 || rank >= world) return fail(TL_ERR_INVALID, "rank %d outside world %d", rank, world);
+  tl_comm* c = new tl_comm;
+  tl_status st = init_common(c, world, device, max_M, max_H);
+  if (st == TL_OK) {
+    c->rank = rank;
+    c->n_local = 1;
+    st = alloc_ws(c, rank);
+  }
+  if (st == TL_OK) {
+    Handle h;
+    memset(&h, 0, sizeof(h));
+    h.magic = kMagic;
+    h.version = 1;
+    h.rank = rank;
+    h.world = world;
+    h.max_M = c->max_M;
+    h.max_H = c->max_H;
+    h.ws_bytes = c->lay.bytes;
+    if (world > 1) {
+      cudaError_t e = cudaIpcGetMemHandle(&h.ipc, c->ws[rank]);
+      if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    }
+    memcpy(my_handle, &h, sizeof(h));
+  }
+  if (st != TL_OK) {
+    tl_comm_destroy(c);
+    return st;
+  }
+  if (world == 1) c->connected = true;
+  *out = c;
+  return TL_OK;
+}
+
+tl_status tl_comm_connect(tl_comm_t c, const void* all_handles) {
+  if (!c || !all_handles) return fail(TL_ERR_INVALID, "null argument");
+  if (c->loopback) return fail(TL_ERR_STATE, "loopback comm needs no connect");
+  if (c->connected) return TL_OK;
+  const Handle* hs = reinterpret_cast<const Handle*>(all_handles);
+  for (int r = 0; r < c->world; ++r) {
+    const Handle& h = hs[r];
+    if (h.magic != kMagic || h.rank != r || h.world != c->world || h.max_M != c->max_M || h.max_H != c->max_H ||
+        h.ws_bytes != c->lay.bytes)
+      return fail(TL_ERR_INVALID, "handle %d does not match this comm (magic/rank/world/capacity)", r);
+  }
+  TL_CUDA(cudaSetDevice(c->device));
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    void* p = nullptr;
+    cudaIpcMemHandle_t ipc = hs[r].ipc;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, ipc, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(TL_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+    c->ws[r] = reinterpret_cast<uint8_t*>(p);
+  }
+  c->connected = true;
+  return TL_OK;
+}
+
+tl_status tl_comm_create_loopback(int world, int device, int64_t max_M, int64_t max_H, tl_comm_t* out) {
+  if (!out) return fail(TL_ERR_INVALID, "null out");
+  *out = nullptr;
+  tl_comm* c = new tl_comm;
+  tl_status st = init_common(c, world, device, max_M, max_H);
+  if (st == TL_OK) {
+    c->loopback = true;
+    c->rank = -1;
+    c->n_local = world;
+    for (int r = 0; r < world && st == TL_OK; ++r) st = alloc_ws(c, r);
+  }
+  if (st != TL_OK) {
+    tl_comm_destroy(c);
+    return st;
+  }
+  c->connected = true;
+  *out = c;
+  return TL_OK;
+}
+
+tl_status tl_comm_destroy(tl_comm_t c) {
+  if (!c) return TL_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < kMaxWorld; ++r) {
+    if (!c->ws[r]) continue;
+    if (c->owned[r]) cudaFree(c->ws[r]);
+    else cudaIpcCloseMemHandle(c->ws[r]);
+  }
+  for (int i = 0; i < kMaxWorld; ++i)
+    if (c->z[i]) cudaFree(c->z[i]);
+  delete c;
+  return TL_OK;
+}
+
+tl_status tl_comm_info(tl_comm_t c, int* rank, int* world, int* local_ranks) {
+  if (!c) return fail(TL_ERR_INVALID, "null comm");
+  if (rank) *rank = c->loopback ? -1 : c->rank;
+  if (world) *world = c->world;
+  if (local_ranks) *local_ranks = c->n_local;
+  return TL_OK;
+}
+
+tl_status tl_set_option(tl_comm_t c, const char* key, int64_t value) {
+  if (!c || !key) return fail(TL_ERR_INVALID, "null argument");
+  for (const auto& d : kOpts)
+    if (!strcmp(d.key, key)) {
+      if (value < d.lo || value > d.hi)
+        return fail(TL_ERR_INVALID, "option %s=%lld outside [%lld, %lld]", key, (long long)value, (long long)d.lo,
+                    (long long)d.hi);
+      c->opt.*(d.field) = value;
+      return TL_OK;
+    }
+  return fail(TL_ERR_INVALID, "unknown option '%s'", key);
+}
+
+tl_status tl_get_option(tl_comm_t c, const char* key, int64_t* value) {
+  if (!c || !key || !value) return fail(TL_ERR_INVALID, "null argument");
+  for (const auto& d : kOpts)
+    if (!strcmp(d.key, key)) {
+      *value = c->opt.*(d.field);
+      return TL_OK;
+    }
+  return fail(TL_ERR_INVALID, "unknown option '%s'", key);
+}
+
+tl_status tl_comm_check(tl_comm_t c, int64_t diag_out[8]) {
+  if (!c) return fail(TL_ERR_INVALID, "null comm");
+  TL_CUDA(cudaSetDevice(c->device));
+  TL_CUDA(cudaDeviceSynchronize());
+  const int r0 = c->loopback ? 0 : c->rank;
+  Diag d;
+  TL_CUDA(cudaMemcpy(&d, c->ws[r0] + c->lay.diag, sizeof(d), cudaMemcpyDeviceToHost));
+  if (diag_out) {
+    const unsigned long long* f = &d.status;
+    for (int i = 0; i < 8; ++i) diag_out[i] = (int64_t)f[i];
+  }
+  if (d.status) {
+    TL_CUDA(cudaMemset(c->ws[r0] + c->lay.diag, 0, sizeof(d)));
+    return fail(TL_ERR_TIMEOUT, "flag wait timed out on rank %llu (kind %llu, src %llu, index %llu, observed %llu, "
+                "expected %llu)", d.rank, d.kind, d.src, d.index, d.observed, d.expected);
+  }
+  return TL_OK;
+}
+
+tl_status tl_ag_gemm(tl_comm_t c, const void* A, const void* B, void* C, void* Ag, int64_t M, int64_t N, int64_t K,
+                     void* stream) {
+  if (c && c->loopback) return fail(TL_ERR_STATE, "loopback comm: use tl_ag_gemm_loopback");
+  void* ag[1] = {Ag};
+  return ag_gemm_impl(c, &A, &B, &C, ag, M, N, K, TL_ACT_NONE, (cudaStream_t)stream);
+}
+
+tl_status tl_ag_gemm_act(tl_comm_t c, const void* A, const void* B, void* C, void* Ag, int64_t M, int64_t N, int64_t K,
+                         tl_act act, void* stream) {
+  if (c && c->loopback) return fail(TL_ERR_STATE, "loopback comm: use tl_ag_gemm_loopback");
+  void* ag[1] = {Ag};
+  return ag_gemm_impl(c, &A, &B, &C, ag, M, N, K, act, (cudaStream_t)stream);
+}
+
+tl_status tl_gemm_rs(tl_comm_t c, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, void* stream) {
+  if (c && c->loopback) return fail(TL_ERR_STATE, "loopback comm: use tl_gemm_rs_loopback");
+  return gemm_rs_impl(c, &A, &B, &C, M, N, K, (cudaStream_t)stream);
+}
+
+tl_status tl_mlp_forward(tl_comm_t c, const void* X, const void* W1, const void* W2, void* out, void* Z, int64_t M,
+                         int64_t H, int64_t I_l, tl_act act, void* stream) {
+  if (c && c->loopback) return fail(TL_ERR_STATE, "loopback comm: use tl_mlp_forward_loopback");
+  void* z[1] = {Z};
+  return mlp_impl(c, &X, &W1, &W2, &out, z, M, H, I_l, act, (cudaStream_t)stream);
+}
+
+tl_status tl_ag_gemm_loopback(tl_comm_t c, const void* const* A, const void* const* B, void* const* C,
+                              void* const* Ag, int64_t M, int64_t N, int64_t K, tl_act act, void* stream) {
+  if (!c || !c->loopback) return fail(TL_ERR_STATE, "not a loopback comm");
+  if (!A || !B || !C) return fail(TL_ERR_INVALID, "null pointer array");
+  return ag_gemm_impl(c, A, B, C, Ag, M, N, K, act, (cudaStream_t)stream);
+}
+
+tl_status tl_gemm_rs_loopback(tl_comm_t c, const void* const* A, const void* const* B, void* const* C, int64_t M,
+                              int64_t N, int64_t K, void* stream) {
+  if (!c || !c->loopback) return fail(TL_ERR_STATE, "not a loopback comm");
+  if (!A || !B || !C) return fail(TL_ERR_INVALID, "null pointer array");
+  return gemm_rs_impl(c, A, B, C, M, N, K, (cudaStream_t)stream);
+}
+
+tl_status tl_mlp_forward_loopback(tl_comm_t c, const void* const* X, const void* const* W1, const void* const* W2,
+                                  void* const* out, void* const* Z, int64_t M, int64_t H, int64_t I_l, tl_act act,
+                                  void* stream) {
+  if (!c || !c->loopback) return fail(TL_ERR_STATE, "not a loopback comm");
+  if (!X || !W1 || !W2 || !out) return fail(TL_ERR_INVALID, "null pointer array");
+  return mlp_impl(c, X, W1, W2, out, Z, M, H, I_l, act, (cudaStream_t)stream);
+}
+
+tl_status tl_debug_static_map(int64_t M, int world, int64_t tm_rows, int channels_per_rank, int64_t n, int64_t* out) {
+  if (!out || M < 1 || world < 1 || world > kMaxWorld || M % world || tm_rows < 1 || n < 0)
+    return fail(TL_ERR_INVALID, "bad arguments");
+  if (n == 0) return TL_OK;
+  StaticMap m = StaticMap::make((int)M, world, (int)std::min<int64_t>(tm_rows, M / world), channels_per_rank);
+  long long* d = nullptr;
+  TL_CUDA(cudaMalloc(&d, (size_t)n * 4 * sizeof(long long)));
+  tl_static_map_kernel<<<64, 256>>>(m, n, d);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(out, d, (size_t)n * 4 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(TL_ERR_CUDA, "static map kernel: %s", cudaGetErrorString(e));
+  return TL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,440 @@
+// tl_kernel.cuh -- the persistent, warp-specialised sm_100a kernel behind tl_ag_gemm,
+// tl_gemm_rs and tl_mlp_forward (SURVEY.md §8(a) rows A0-B3').
+//
+// One CTA per SM (or CTA pair on a TPC with tcgen05 cta_group::2), 8 warps:
+//   warp 0      TMA producer.  AG: consumer_tile_wait on the producer tiles its A rows need
+//               (P:242-243), then TMA loads of A / B k-blocks into a smem ring.
+//   warp 1      MMA issuer (pair leader only): tcgen05.mma 128|256 x 256 x 16 into a
+//               double-buffered TMEM accumulator (2 x 256 fp32 columns).
+//   warp 2      TMEM allocator.
+//   warp 3      AG copy role (tile_push_data broadcast over (tile, destination) tasks):
+//               bulk-copy each producer tile of the local shard into every rank's X_full
+//               (NVLink peer stores) and producer_tile_notify it there.
+//   warps 4-7   epilogue: tcgen05.ld -> (SiLU/GeLU)*up | RS push | RS owner reduce -> bf16 ->
+//               swizzled smem -> TMA store.  GEMM-RS: tiles of a remote owner are pushed into the
+//               owner's staging slot and peer_tile_notify'd; the owner's
+//               own tiles peer_tile_wait on every slot and reduce in fp32 in ascending rank order.
+// Communication tile (Tm_p rows) and compute tile (128*kPair x 256) are chosen independently
+// (the decoupled design space).
+#pragma once
+#include "tl_params.h"
+#include "tl_primitives.cuh"
+#include "tl_ptx.cuh"
+
+namespace tl {
+
+constexpr int kThreads = 256;
+constexpr int kBK = 64;                    // K per stage (one 128-byte swizzle row of bf16)
+constexpr int kUmmaN = 256;                // accumulator columns per tile
+constexpr int kAStage = 128 * kBK * 2;     // 16 KB: 128 rows of A per CTA
+constexpr int kEpiBytes = 4 * 2 * 4096;    // 4 warps x 2 buffers x (32 rows x 128 B)
+constexpr int kCopyPiece = 16384;          // AG bulk-copy piece (bytes)
+constexpr int kCopyBytes = 2 * kCopyPiece;
+
+template <int kPair, int kStages, bool kAG>
+struct Layout {
+  static constexpr int kBStage = (kPair == 2 ? 128 : 256) * kBK * 2;
+  static constexpr int off_a = 0;
+  static constexpr int off_b = off_a + kStages * kAStage;
+  static constexpr int off_epi = off_b + kStages * kBStage;
+  static constexpr int off_copy = off_epi + kEpiBytes;
+  static constexpr int off_bar = off_copy + (kAG ? kCopyBytes : 0);
+  // full[S], empty[S], tfull[2], tempty[2], copy[2]
+  static constexpr int n_bars = 2 * kStages + 6;
+  static constexpr int off_tmem = off_bar + n_bars * 8;
+  static constexpr int bytes = off_tmem + 16;
+  static constexpr int smem_request = bytes + 1024;  // slack for manual 1024-byte alignment
+};
+
+__host__ __device__ constexpr int stages_for(int pair, bool ag) {
+  return pair == 2 ? (ag ? 5 : 6) : (ag ? 3 : 4);
+}
+
+// Schedule index j -> m-block (tile order subspace).
+__device__ __forceinline__ int m_perm(const Params& p, int rank, int m_rot, int j) {
+  if (p.order == ORDER_AG_INTERLEAVE) {
+    // own rows first, then block `loc` of every other rank in ring order (r+1, r+2, ...):
+    // matches the copy role's tile-major push order, so blocks arrive roughly in this order.
+    const int bpr = p.m_blocks / p.world;
+    if (j < bpr) return rank * bpr + j;
+    const int jj = j - bpr, loc = jj / (p.world - 1), s = (rank + 1 + jj % (p.world - 1)) % p.world;
+    return s * bpr + loc;
+  }
+  if (p.order == ORDER_ROTATE) return (j + m_rot) % p.m_blocks;
+  return j;
+}
+
+// Tile t of the persistent schedule -> (m-block, n-block), grouped rasterisation so that the
+// ~74 concurrently running tiles share A and B blocks in L2.
+__device__ __forceinline__ void tile_coords(const Params& p, int rank, int m_rot, int t, int& mb, int& nb) {
+  const int G = p.raster_group;
+  const int per_group = G * p.n_blocks;
+  const int group = t / per_group;
+  const int first = group * G;
+  const int rows = min(G, p.m_blocks - first);
+  const int local = t - group * per_group;
+  nb = local / rows;
+  mb = m_perm(p, rank, m_rot, first + local % rows);
+}
+
+// consumer_tile_wait for A rows [lo, hi) of the gathered tensor: every producer tile of every
+// channel those rows span must carry this call's epoch.
+__device__ __forceinline__ void ag_wait_rows(const Params& p, int rank, int lo, int hi) {
+  const uint32_t* flags = p.ag_flags[rank];
+  for (int s = lo / p.M_r; s <= (hi - 1) / p.M_r; ++s) {
+    const int a = max(lo, s * p.M_r) - s * p.M_r;
+    const int b = min(hi, (s + 1) * p.M_r) - s * p.M_r;
+    const int c0 = (a / p.tm_rows) / p.tiles_per_channel;
+    const int c1 = ((b - 1) / p.tm_rows) / p.tiles_per_channel;
+    const int t_end = min((c1 + 1) * p.tiles_per_channel, p.tiles_per_rank);
+    for (int t = c0 * p.tiles_per_channel; t < t_end; ++t)
+      tile_wait(flags + s * kAgFlagStride + t, p.epoch, p.timeout_ns, p.diag, rank, 1, s, t);
+  }
+}
+
+// Convert 64 fp32 values of this thread's row to bf16, write them into the warp's swizzled
+// 32 x 128 B staging buffer and TMA-store the 64 x 32 box at (col, row).
+__device__ __forceinline__ void store_chunk(const float* v, uint8_t* bufs, int& sbuf, const CUtensorMap* tm,
+                                            int col, int row, uint32_t lane) {
+  uint8_t* buf = bufs + sbuf * 4096;
+  if (lane == 0) ptx::bulk_wait_read<1>();
+  __syncwarp();
+  const uint32_t row_addr = ptx::smem_u32(buf) + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    ptx::st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), ptx::pack_bf16x2(v[8 * j + 0], v[8 * j + 1]),
+                      ptx::pack_bf16x2(v[8 * j + 2], v[8 * j + 3]), ptx::pack_bf16x2(v[8 * j + 4], v[8 * j + 5]),
+                      ptx::pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+  }
+  ptx::fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    ptx::tma_store_2d(tm, buf, col, row);
+    ptx::bulk_commit();
+  }
+  sbuf ^= 1;
+}
+
+// acc[0..63] += bf16 slot row segment (8 x 16 B), columns beyond N skipped (N % 8 == 0).
+__device__ __forceinline__ void add_slot_row(float* acc, const uint16_t* rowp, int col, int N) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (col + 8 * j < N) {
+      const uint4 q = ptx::ld_global_v4(rowp + col + 8 * j);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc[8 * j + 2 * e] += __uint_as_float(w[e] << 16);
+        acc[8 * j + 2 * e + 1] += __uint_as_float(w[e] & 0xFFFF0000u);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
+__device__ __forceinline__ float gelu_tanh_f(float g) {
+  return 0.5f * g * (1.0f + tanhf(0.7978845608028654f * (g + 0.044715f * g * g * g)));
+}
+
+template <int kPair, int kStages, int kEpi, bool kAG>
+__global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_constant__ Params p) {
+  using L = Layout<kPair, kStages, kAG>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int lr = blockIdx.x / p.ctas_per_rank;              // local rank slot of this CTA
+  const int cta_in_rank = blockIdx.x % p.ctas_per_rank;
+  const int cta_in_pair = kPair == 2 ? (int)ptx::cluster_ctarank() : 0;
+  const int pair = cta_in_rank / kPair, n_pairs = p.ctas_per_rank / kPair;
+  const RankArgs& ra = p.rk[lr];
+  const int rank = ra.rank;
+  const int total = p.m_blocks * p.n_blocks;
+  constexpr int BM = 128 * kPair;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* tfull = bars + 2 * kStages;
+  uint64_t* tempty = bars + 2 * kStages + 2;
+  uint64_t* cbar = bars + 2 * kStages + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::off_tmem);
+
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], kPair);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], 4 * kPair);
+      ptx::mbar_init(&cbar[s], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&ra.tm_a);
+    ptx::prefetch_tmap(&ra.tm_b0);
+    if (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) ptx::prefetch_tmap(&ra.tm_b1);
+  }
+  if (warp == 2) ptx::tmem_alloc<kPair>(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  if constexpr (kPair == 2) ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ============================== TMA producer ==============================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < total; t += n_pairs) {
+        int mb, nb;
+        tile_coords(p, rank, ra.m_rot, t, mb, nb);
+        const int row0 = mb * BM + cta_in_pair * 128;
+        if constexpr (kAG) {
+          if (row0 < p.M) ag_wait_rows(p, rank, row0, min(row0 + 128, p.M));
+        }
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + L::off_a + stage * kAStage;
+          uint8_t* sb = smem + L::off_b + stage * L::kBStage;
+          const int kc = kb * kBK;
+          if constexpr (kPair == 2) {
+            ptx::tma_load_2d_pair(&ra.tm_a, &full[stage], sa, kc, row0);
+            if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL)
+              ptx::tma_load_2d_pair(cta_in_pair == 0 ? &ra.tm_b0 : &ra.tm_b1, &full[stage], sb, kc, nb * 128);
+            else
+              ptx::tma_load_2d_pair(&ra.tm_b0, &full[stage], sb, kc, nb * kUmmaN + cta_in_pair * 128);
+          } else {
+            ptx::tma_load_2d(&ra.tm_a, &full[stage], sa, kc, row0);
+            if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) {
+              ptx::tma_load_2d(&ra.tm_b0, &full[stage], sb, kc, nb * 128);
+              ptx::tma_load_2d(&ra.tm_b1, &full[stage], sb + 128 * 128, kc, nb * 128);
+            } else {
+              ptx::tma_load_2d(&ra.tm_b0, &full[stage], sb, kc, nb * kUmmaN);
+            }
+          }
+          if (cta_in_pair == 0)
+            ptx::mbar_arrive_expect_tx(&full[stage], (kAStage + L::kBStage) * kPair);
+          else
+            ptx::mbar_arrive_cluster(&full[stage], 0);
+          if (++stage == kStages) stage = 0, phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================== MMA issuer ==============================
+    if (cta_in_pair == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(128 * kPair, kUmmaN);
+      int stage = 0, it = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < total; t += n_pairs, ++it) {
+        const int as = it & 1;
+        ptx::mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t tmem_d = tmem_base + as * kUmmaN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(smem + L::off_a + stage * kAStage));
+            const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(smem + L::off_b + stage * L::kBStage));
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              ptx::mma_bf16<kPair>(ad + 2 * k, bd + 2 * k, tmem_d, idesc, (kb | k) != 0);
+            ptx::mma_commit<kPair>(&empty[stage]);
+            if (kb == p.k_blocks - 1) ptx::mma_commit<kPair>(&tfull[as]);
+          }
+          __syncwarp();
+          if (++stage == kStages) stage = 0, phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ============================== AG copy role ==============================
+    if constexpr (kAG) {
+      if (lane == 0 && cta_in_rank < p.copy_ctas) {
+        uint8_t* cbuf = smem + L::off_copy;
+        uint32_t cph[2] = {0, 0};
+        int g = 0;  // global piece counter -> buffer g & 1
+        const int W = p.world;
+        const int n_tasks = p.tiles_per_rank * W;
+        for (int task = cta_in_rank; task < n_tasks; task += p.copy_ctas) {
+          const int t = task / W, d = (rank + task % W) % W;  // tile-major, self first, then r+1, ...
+          const int lo = t * p.tm_rows, hi = min(lo + p.tm_rows, p.M_r);
+          const uint32_t bytes = (uint32_t)(hi - lo) * (uint32_t)p.row_bytes;
+          const uint8_t* src = ra.a_shard + (size_t)lo * p.row_bytes;
+          uint8_t* dst = p.xfull[d] + ((size_t)rank * p.M_r + lo) * p.row_bytes;
+          const int n = (int)((bytes + kCopyPiece - 1) / kCopyPiece);
+          for (int i = 0; i < n; ++i) {
+            const int b = (g + i) & 1;
+            const uint32_t sz = min((uint32_t)kCopyPiece, bytes - (uint32_t)i * kCopyPiece);
+            if (i == 0) {
+              ptx::mbar_arrive_expect_tx(&cbar[b], sz);
+              ptx::bulk_load(cbuf + b * kCopyPiece, src, sz, &cbar[b]);
+            }
+            if (i + 1 < n) {  // prefetch the next piece into the other buffer once its store has read it
+              const uint32_t sz1 = min((uint32_t)kCopyPiece, bytes - (uint32_t)(i + 1) * kCopyPiece);
+              ptx::bulk_wait_read<0>();
+              ptx::mbar_arrive_expect_tx(&cbar[b ^ 1], sz1);
+              ptx::bulk_load(cbuf + (b ^ 1) * kCopyPiece, src + (size_t)(i + 1) * kCopyPiece, sz1, &cbar[b ^ 1]);
+            }
+            ptx::mbar_wait(&cbar[b], cph[b]);
+            cph[b] ^= 1;
+            ptx::bulk_store(dst + (size_t)i * kCopyPiece, cbuf + b * kCopyPiece, sz);
+            ptx::bulk_commit();
+          }
+          g += n;
+          ptx::bulk_wait<0>();  // every byte of this producer tile has landed at rank d
+          const bool drop = rank == p.drop_rank && t == p.drop_index && d == (rank + 1) % W;
+          if (!drop) tile_notify(p.ag_flags[d] + rank * kAgFlagStride + t, p.epoch);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ============================== epilogue ==============================
+    const int ew = warp - 4;
+    uint8_t* bufs = smem + L::off_epi + ew * 8192;
+    int sbuf = 0, it = 0;
+    for (int t = pair; t < total; t += n_pairs, ++it) {
+      int mb, nb;
+      tile_coords(p, rank, ra.m_rot, t, mb, nb);
+      const int as = it & 1;
+      ptx::mbar_wait(&tfull[as], (it >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t tacc = tmem_base + as * kUmmaN + ((uint32_t)(ew * 32) << 16);
+      const int row0 = mb * BM + cta_in_pair * 128;  // first row of this CTA's half-tile
+      auto release_tmem = [&]() {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(&tempty[as], 0);
+      };
+      float v[64];
+      if constexpr (kEpi == EPI_STORE) {
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          ptx::tmem_ld32(tacc + c * 64, v);
+          ptx::tmem_ld32(tacc + c * 64 + 32, v + 32);
+          ptx::tmem_ld_wait();
+          if (c == 3) release_tmem();
+          store_chunk(v, bufs, sbuf, &ra.tm_c, nb * kUmmaN + c * 64, row0 + ew * 32, lane);
+        }
+      } else if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) {
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          float u[64];
+          ptx::tmem_ld32(tacc + c * 64, v);
+          ptx::tmem_ld32(tacc + c * 64 + 32, v + 32);
+          ptx::tmem_ld32(tacc + 128 + c * 64, u);
+          ptx::tmem_ld32(tacc + 128 + c * 64 + 32, u + 32);
+          ptx::tmem_ld_wait();
+          if (c == 1) release_tmem();
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            v[i] = (kEpi == EPI_SILU_MUL ? silu_f(v[i]) : gelu_tanh_f(v[i])) * u[i];
+          store_chunk(v, bufs, sbuf, &ra.tm_c, nb * 128 + c * 64, row0 + ew * 32, lane);
+        }
+      } else if (row0 >= p.M) {
+        release_tmem();                              // half-tile past the last row: nothing to do
+      } else {
+        // ---------------- GEMM-RS epilogue ----------------
+        const int W = p.world;
+        const int o = row0 / p.M_r;                 // owner of these rows (offset in the global view)
+        const int lrow0 = row0 - o * p.M_r;         // first row inside the owner's block
+        const int tile = (lrow0 / 128) * p.n_blocks + nb;
+        const int myrow = lrow0 + ew * 32 + (int)lane;
+        const uint16_t* stg = p.staging[rank];
+        bool push;
+        int tgt = 0, slot = 0;                       // push target rank and slot
+        if (p.rs_mode == RS_RING) {
+          const int step = (o - rank - 1 + 2 * W) % W;   // o = r+1 -> 0, ..., o = r -> W-1
+          if (step > 0) {                            // peer_tile_wait on the partial from rank r+1
+            if (lane == 0)
+              tile_wait(p.rs_flags[rank] + o * kRsFlagStride + tile, p.epoch, p.timeout_ns, p.diag, rank, 2,
+                        (rank + 1) % W, tile);
+            __syncwarp();
+          }
+          push = step < W - 1;
+          tgt = (rank - 1 + W) % W;
+          slot = o;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            ptx::tmem_ld32(tacc + c * 64, v);
+            ptx::tmem_ld32(tacc + c * 64 + 32, v + 32);
+            ptx::tmem_ld_wait();
+            if (c == 3) release_tmem();
+            const int col = nb * kUmmaN + c * 64;
+            if (step > 0) add_slot_row(v, stg + ((size_t)o * p.M_r + myrow) * p.N_out, col, p.N_out);
+            if (push)
+              store_chunk(v, bufs, sbuf, &p.tm_stage[tgt], col, slot * p.M_r + lrow0 + ew * 32, lane);
+            else
+              store_chunk(v, bufs, sbuf, &ra.tm_c, col, lrow0 + ew * 32, lane);
+          }
+        } else {
+          push = o != rank;
+          tgt = o;
+          slot = rank;
+          if (!push) {                               // owner: peer_tile_wait on every other slot
+            if ((int)lane < W && (int)lane != rank)
+              tile_wait(p.rs_flags[rank] + lane * kRsFlagStride + tile, p.epoch, p.timeout_ns, p.diag, rank, 2,
+                        lane, tile);
+            __syncwarp();
+          }
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            ptx::tmem_ld32(tacc + c * 64, v);
+            ptx::tmem_ld32(tacc + c * 64 + 32, v + 32);
+            ptx::tmem_ld_wait();
+            if (c == 3) release_tmem();
+            const int col = nb * kUmmaN + c * 64;
+            if (push) {
+              store_chunk(v, bufs, sbuf, &p.tm_stage[tgt], col, slot * p.M_r + lrow0 + ew * 32, lane);
+            } else {
+              for (int s = 0; s < W; ++s)            // own fp32 partial + slots, ascending rank
+                if (s != rank) add_slot_row(v, stg + ((size_t)s * p.M_r + myrow) * p.N_out, col, p.N_out);
+              store_chunk(v, bufs, sbuf, &ra.tm_c, col, lrow0 + ew * 32, lane);
+            }
+          }
+        }
+        if (push) {
+          // every byte of this half-tile has landed in the target's slot -> notify (release)
+          if (lane == 0) ptx::bulk_wait<0>();
+          __syncwarp();
+          ptx::named_bar_sync(1, 128);
+          if (ew == 0 && lane == 0)
+            tile_notify(p.rs_flags[tgt] + slot * kRsFlagStride + tile, p.epoch);
+        }
+      }
+    }
+    if (lane == 0) ptx::bulk_wait<0>();
+    __syncwarp();
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if constexpr (kPair == 2) ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<kPair>(tmem_base, 512);
+  }
+}
+
+// Writes zeros to a [rows, cols] bf16 matrix (the K == 0 degenerate product).
+__global__ void tl_zero_kernel(uint16_t* out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = 0;
+}
+
+// Device-side evaluation of the static mapping for the index tests.
+__global__ void tl_static_map_kernel(StaticMap m, long long n, long long* out) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    out[4 * t + 0] = m.f_S_lo((int)t);
+    out[4 * t + 1] = m.f_S_hi((int)t);
+    out[4 * t + 2] = m.f_R((int)t);
+    out[4 * t + 3] = m.f_C((int)t);
+  }
+}
+
+}  // namespace tl

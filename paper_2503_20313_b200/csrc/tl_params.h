@@ -1,0 +1,50 @@
+// tl_params.h -- launch parameters shared by the host launcher (tl_api.cu) and the kernels.
+// The `BlockChannel` analogue of the paper ("current process rank, total world size,
+// synchronization barrier configurations, and producer/consumer block relationships").
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+
+#include "tl_primitives.cuh"
+
+namespace tl {
+
+constexpr int kMaxWorld = 8;
+constexpr int kAgFlagStride = 4096;   // producer tiles per source rank (flags per source)
+constexpr int kRsFlagStride = 16384;  // CTA tiles per owner block (flags per slot)
+
+enum Epi : int { EPI_STORE = 0, EPI_SILU_MUL = 1, EPI_GELU_MUL = 2, EPI_RS = 3 };
+enum Order : int { ORDER_IDENTITY = 0, ORDER_AG_INTERLEAVE = 1, ORDER_ROTATE = 2 };
+enum RsMode : int { RS_NONE = 0, RS_ONESHOT = 1, RS_RING = 2 };
+
+// Per rank driven by this launch (1 entry for a process-per-GPU comm, `world` for loopback).
+struct alignas(64) RankArgs {
+  CUtensorMap tm_a;   // A operand [M, K]: gathered X_full bank (AG, world > 1) or the caller's A
+  CUtensorMap tm_b0;  // B rows [N, K] (plain) or the gate rows [N_out, K] (gated)
+  CUtensorMap tm_b1;  // up rows [N_out, K] (gated only)
+  CUtensorMap tm_c;   // output [rows, N_out] store target, 64 x 32 boxes
+  const uint8_t* a_shard;  // AG copy source: this rank's [M/world, K] shard
+  int rank;
+  int m_rot;          // first schedule m-block (ORDER_ROTATE)
+};
+
+struct alignas(64) Params {
+  RankArgs rk[kMaxWorld];
+  CUtensorMap tm_stage[kMaxWorld];   // RS: staging bank of rank o viewed as [world * M_r, N]
+  uint8_t* xfull[kMaxWorld];         // AG: current X_full bank of rank d (local or NVLink peer)
+  uint32_t* ag_flags[kMaxWorld];     // AG: [src][kAgFlagStride] producer-tile flags of rank d
+  uint32_t* rs_flags[kMaxWorld];     // RS: [slot][kRsFlagStride] partial-tile flags of rank o
+  const uint16_t* staging[kMaxWorld];// RS: current staging bank of rank o, [world][M_r][N] bf16
+  Diag* diag;                        // device-side timeout record (first writer wins)
+  uint64_t timeout_ns;
+  int M, N_out, K, M_r, world, n_local, ctas_per_rank;
+  int m_blocks, n_blocks, k_blocks, raster_group, order;
+  uint32_t epoch;
+  // AG (producer = copy role, consumer = GEMM A loads)
+  int tm_rows, tiles_per_rank, tiles_per_channel, copy_ctas, row_bytes;
+  // RS
+  int rs_mode;
+  int drop_rank, drop_index;
+};
+
+}  // namespace tl

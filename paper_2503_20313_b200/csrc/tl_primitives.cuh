@@ -1,0 +1,104 @@
+// tl_primitives.cuh -- the paper's tile-centric primitives (PAPER.md Table "Tile-centric
+// primitives") and static tile-centric mapping, B200 edition.
+//
+// Signals are u32 flags in symmetric (IPC-shared) device memory, each with exactly one writer,
+// holding the host epoch of the call that last set them.  A notify is a sys-scope release
+// store of the current epoch; a wait is a sys-scope acquire spin until the flag is >= the
+// epoch (monotone, so flags are never reset and a stale flag from an earlier call can never
+// satisfy a later wait).  Data primitives move tiles with the SM's bulk-copy (TMA) engine
+// straight to NVLink peer addresses.
+#pragma once
+#include "tl_ptx.cuh"
+
+namespace tl {
+
+// Static mapping for producer (communication) tiles of the AllGather, Sec. 4.1.
+// M rows are row-sharded over R ranks (M_per_rank = M / R, the ABI requires R | M); each rank's
+// rows are cut into producer tiles of Tm rows (the last tile of a rank clamped) and
+// grouped into C channels of `tiles_per_channel` consecutive tiles.  When Tm | M_per_rank and
+// C | (M_per_rank / Tm) these are exactly the paper's affine formulas
+//   range_M = [t Tm, t Tm + Tm),  src_rank = floor(t / floor(M_per_rank / Tm)),
+//   channel = floor(t / floor(M_per_channel / Tm)),  M_per_channel = M / (R C);
+// otherwise tiles never straddle ranks (reading R4).
+struct StaticMap {
+  int M, R, M_r, Tm, tiles_per_rank, tiles_per_channel, channels_per_rank;
+
+  __host__ __device__ static StaticMap make(int M, int R, int Tm, int C /* 0 = one tile per channel */) {
+    StaticMap s;
+    s.M = M;
+    s.R = R;
+    s.M_r = M / R;
+    s.Tm = Tm;
+    s.tiles_per_rank = (s.M_r + Tm - 1) / Tm;
+    if (C <= 0 || C > s.tiles_per_rank) C = s.tiles_per_rank;
+    s.tiles_per_channel = (s.tiles_per_rank + C - 1) / C;
+    s.channels_per_rank = (s.tiles_per_rank + s.tiles_per_channel - 1) / s.tiles_per_channel;
+    return s;
+  }
+  // f_R: producer tile (global id) -> source rank
+  __host__ __device__ int f_R(int t) const { return t / tiles_per_rank; }
+  // f_S: producer tile -> [row_lo, row_hi) in the gathered tensor
+  __host__ __device__ int f_S_lo(int t) const { return f_R(t) * M_r + (t % tiles_per_rank) * Tm; }
+  __host__ __device__ int f_S_hi(int t) const {
+    int lo = f_S_lo(t), end = (f_R(t) + 1) * M_r;
+    return lo + Tm < end ? lo + Tm : end;
+  }
+  // f_C: producer tile -> global barrier channel in [0, R * channels_per_rank)
+  __host__ __device__ int f_C(int t) const {
+    return f_R(t) * channels_per_rank + (t % tiles_per_rank) / tiles_per_channel;
+  }
+};
+
+// Timeout record written by the first wait that gives up (tl_comm_check reads it).
+struct Diag {
+  unsigned long long status, rank, kind, src, index, observed, expected, epoch;
+};
+
+// Spin (acquire) until *flag >= epoch.  Never hangs: past `timeout_ns` it records the wait in
+// `diag` (first one wins) and returns false so the kernel can drain and exit.
+__device__ __forceinline__ bool flag_wait(const uint32_t* flag, uint32_t epoch, uint64_t timeout_ns, Diag* diag,
+                                          int rank, int kind, int src, int index) {
+  uint32_t v = ptx::ld_acquire_sys(flag);
+  if (v >= epoch) return true;
+  const uint64_t t0 = ptx::globaltimer();
+  uint32_t n = 0;
+  while ((v = ptx::ld_acquire_sys(flag)) < epoch) {
+    if ((++n & 63u) == 0) {
+      if (ptx::globaltimer() - t0 > timeout_ns) {
+        if (atomicCAS(&diag->status, 0ull, 4ull) == 0ull) {
+          diag->rank = rank;
+          diag->kind = kind;
+          diag->src = src;
+          diag->index = index;
+          diag->observed = v;
+          diag->expected = epoch;
+          diag->epoch = epoch;
+          __threadfence_system();
+        }
+        return false;
+      }
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
+// producer_tile_notify(tile_id, p2p) / peer_tile_notify(tile_id, rank): release the
+// epoch into the single flag owned by (tile, target rank).  All data the calling thread (and,
+// through the preceding barrier, its CTA) wrote before -- including async-proxy bulk/TMA
+// stores whose groups were waited on -- becomes visible to the acquirer.
+__device__ __forceinline__ void tile_notify(uint32_t* flag, uint32_t epoch) {
+  ptx::fence_proxy_async_global();
+  ptx::st_release_sys(flag, epoch);
+}
+
+// consumer_tile_wait / peer_tile_wait: acquire, then order later async-proxy (TMA)
+// reads after it.
+__device__ __forceinline__ bool tile_wait(const uint32_t* flag, uint32_t epoch, uint64_t timeout_ns, Diag* diag,
+                                          int rank, int kind, int src, int index) {
+  bool ok = flag_wait(flag, epoch, timeout_ns, diag, rank, kind, src, index);
+  ptx::fence_proxy_async_global();
+  return ok;
+}
+
+}  // namespace tl
