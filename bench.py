@@ -217,14 +217,17 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # clocks are sampled (nvidia-smi, 100 ms) from before the warm-up, through the timed region and
+    # a ~1 s soak of the same step afterwards, so the samples see the GPU under this exact load
+    clocks = Clocks(dev)
+    clocks.start()
+    time.sleep(0.3)
     for _ in range(args.warmup):
         step()
     barrier()
 
     # ---- timed region: K steps, per-kernel CUDA events on the launching stream
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    clocks = Clocks(dev)
-    clocks.start()
     barrier()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -237,6 +240,11 @@ def main():
         ev[i][2].record(stream)
     t_end.record(stream)
     barrier()
+    soak_end = time.perf_counter() + 1.0
+    while time.perf_counter() < soak_end:
+        for _ in range(8):
+            step()
+        torch.cuda.synchronize()
     clk = clocks.stop()
     total_ms = max_over_ranks(t_start.elapsed_time(t_end))
     k1 = [e[0].elapsed_time(e[1]) for e in ev]

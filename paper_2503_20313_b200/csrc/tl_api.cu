@@ -271,8 +271,9 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
     return fail(TL_ERR_INVALID, "M=%lld K=%lld exceed comm capacity (%lld, %lld)", (long long)M, (long long)K,
                 (long long)c->max_M, (long long)c->max_H);
   if (M >= (1ll << 31) || N_out >= (1ll << 31) || K >= (1ll << 31)) return fail(TL_ERR_UNSUPPORTED, "dimension >= 2^31");
-  for (int i = 0; i < c->n_local; ++i) {
-    if (!A[i] || !B[i] || !C[i]) return fail(TL_ERR_INVALID, "null pointer (rank slot %d)", i);
+  for (int i = 0; i < c->n_local; ++i) {   // a pointer may be null only when its tensor is empty
+    if ((!A[i] && M * K) || (!B[i] && N_out * K) || (!C[i] && M * N_out))
+      return fail(TL_ERR_INVALID, "null pointer (rank slot %d)", i);
     if (!aligned16(A[i]) || !aligned16(B[i]) || !aligned16(C[i]) || (Agath && Agath[i] && !aligned16(Agath[i])))
       return fail(TL_ERR_INVALID, "pointers must be 16-byte aligned");
   }
@@ -380,7 +381,8 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
     if ((M_r / 128) * n_blocks > kRsFlagStride) return fail(TL_ERR_UNSUPPORTED, "too many RS tiles per owner block");
   }
   for (int i = 0; i < c->n_local; ++i) {
-    if (!A[i] || !B[i] || !C[i]) return fail(TL_ERR_INVALID, "null pointer (rank slot %d)", i);
+    if ((!A[i] && M * K) || (!B[i] && N * K) || (!C[i] && M_r * N))
+      return fail(TL_ERR_INVALID, "null pointer (rank slot %d)", i);
     if (!aligned16(A[i]) || !aligned16(B[i]) || !aligned16(C[i])) return fail(TL_ERR_INVALID, "pointers must be 16-byte aligned");
   }
   if (M == 0 || N == 0) return TL_OK;
