@@ -89,7 +89,7 @@ def test_validation_errors(tl):
     with pytest.raises(TLError, match="INVALID"):          # over capacity
         c.ag_gemm_lb([cuda(torch.zeros(512, 64).bfloat16())] * 2, Bs, [empty(1024, 64)] * 2)
     with pytest.raises(TLError, match="INVALID"):          # misaligned pointer
-        big = empty(4096)
+        big = empty(64 * 64 + 8)
         c.ag_gemm_lb([big[1:1 + 64 * 64].view(64, 64)] * 2, Bs, Cs)
     with pytest.raises(TLError, match="INVALID"):
         c.set_option("rs_order", 7)
