@@ -107,7 +107,8 @@ tl_status make_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t col
 
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
-          raster_group = 8, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1;
+          raster_group = 8, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
+          n_sub = 0;
 };
 
 struct OptDesc {
@@ -126,6 +127,7 @@ const OptDesc kOpts[] = {
     {"timeout_ms", &Options::timeout_ms, 1, 1ll << 40},
     {"debug_drop_notify", &Options::debug_drop_notify, -1, 1 << 30},
     {"debug_drop_rank", &Options::debug_drop_rank, -1, kMaxWorld - 1},
+    {"n_sub", &Options::n_sub, 0, 2},
 };
 
 }  // namespace
@@ -191,11 +193,11 @@ int ctas_per_rank(const tl_comm* c) {
   return n < pair ? pair : n;
 }
 
-template <int kPair, int kEpi, bool kAG>
+template <int kPair, int kEpi, bool kAG, int kNSub>
 tl_status launch_t(tl_comm* c, const Params& p, cudaStream_t stream) {
-  constexpr int kStages = stages_for(kPair, kAG);
-  using L = Layout<kPair, kStages, kAG>;
-  auto kern = tl_gemm_kernel<kPair, kStages, kEpi, kAG>;
+  constexpr int kStages = stages_for(kPair, kAG, kNSub);
+  using L = Layout<kPair, kStages, kAG, kNSub>;
+  auto kern = tl_gemm_kernel<kPair, kStages, kEpi, kAG, kNSub>;
   static bool attr_set = false;
   if (!attr_set) {
     TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::smem_request));
@@ -217,22 +219,54 @@ tl_status launch_t(tl_comm* c, const Params& p, cudaStream_t stream) {
   return TL_OK;
 }
 
-tl_status launch(tl_comm* c, const Params& p, int epi, bool ag, cudaStream_t s) {
+tl_status launch(tl_comm* c, const Params& p, int epi, bool ag, int nsub, cudaStream_t s) {
   const int pair = pair_of(c);
-  if (pair == 2) {
-    if (epi == EPI_STORE) return ag ? launch_t<2, EPI_STORE, true>(c, p, s) : launch_t<2, EPI_STORE, false>(c, p, s);
+  if (pair == 2 && nsub == 2) {
+    if (epi == EPI_STORE) return ag ? launch_t<2, EPI_STORE, true, 2>(c, p, s) : launch_t<2, EPI_STORE, false, 2>(c, p, s);
     if (epi == EPI_SILU_MUL)
-      return ag ? launch_t<2, EPI_SILU_MUL, true>(c, p, s) : launch_t<2, EPI_SILU_MUL, false>(c, p, s);
+      return ag ? launch_t<2, EPI_SILU_MUL, true, 2>(c, p, s) : launch_t<2, EPI_SILU_MUL, false, 2>(c, p, s);
     if (epi == EPI_GELU_MUL)
-      return ag ? launch_t<2, EPI_GELU_MUL, true>(c, p, s) : launch_t<2, EPI_GELU_MUL, false>(c, p, s);
-    return launch_t<2, EPI_RS, false>(c, p, s);
+      return ag ? launch_t<2, EPI_GELU_MUL, true, 2>(c, p, s) : launch_t<2, EPI_GELU_MUL, false, 2>(c, p, s);
+    return launch_t<2, EPI_RS, false, 2>(c, p, s);
   }
-  if (epi == EPI_STORE) return ag ? launch_t<1, EPI_STORE, true>(c, p, s) : launch_t<1, EPI_STORE, false>(c, p, s);
+  if (pair == 2) {
+    if (epi == EPI_STORE) return ag ? launch_t<2, EPI_STORE, true, 1>(c, p, s) : launch_t<2, EPI_STORE, false, 1>(c, p, s);
+    if (epi == EPI_SILU_MUL)
+      return ag ? launch_t<2, EPI_SILU_MUL, true, 1>(c, p, s) : launch_t<2, EPI_SILU_MUL, false, 1>(c, p, s);
+    if (epi == EPI_GELU_MUL)
+      return ag ? launch_t<2, EPI_GELU_MUL, true, 1>(c, p, s) : launch_t<2, EPI_GELU_MUL, false, 1>(c, p, s);
+    return launch_t<2, EPI_RS, false, 1>(c, p, s);
+  }
+  if (epi == EPI_STORE) return ag ? launch_t<1, EPI_STORE, true, 1>(c, p, s) : launch_t<1, EPI_STORE, false, 1>(c, p, s);
   if (epi == EPI_SILU_MUL)
-    return ag ? launch_t<1, EPI_SILU_MUL, true>(c, p, s) : launch_t<1, EPI_SILU_MUL, false>(c, p, s);
+    return ag ? launch_t<1, EPI_SILU_MUL, true, 1>(c, p, s) : launch_t<1, EPI_SILU_MUL, false, 1>(c, p, s);
   if (epi == EPI_GELU_MUL)
-    return ag ? launch_t<1, EPI_GELU_MUL, true>(c, p, s) : launch_t<1, EPI_GELU_MUL, false>(c, p, s);
-  return launch_t<1, EPI_RS, false>(c, p, s);
+    return ag ? launch_t<1, EPI_GELU_MUL, true, 1>(c, p, s) : launch_t<1, EPI_GELU_MUL, false, 1>(c, p, s);
+  return launch_t<1, EPI_RS, false, 1>(c, p, s);
+}
+
+// Number of 256-column MMA sub-tiles per tile (option n_sub, 0 = auto): 512-wide tiles move 25 %
+// fewer bytes per FLOP but quantise N and the wave count more coarsely and serialise the epilogue.
+int choose_nsub(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gated) {
+  if (pair_of(c) != 2) return 1;
+  if (c->opt.n_sub == 1 || c->opt.n_sub == 2) return (int)c->opt.n_sub;
+  const int n_pairs = ctas_per_rank(c) / 2;
+  const int64_t m_blocks = (M + 255) / 256;
+  double best = -1;
+  int pick = 1;
+  for (int ns = 1; ns <= 2; ++ns) {
+    const int64_t bn = (gated ? 128 : 256) * ns;
+    const int64_t nb = (N_out + bn - 1) / bn;
+    const int64_t tiles = m_blocks * nb;
+    const int64_t waves = (tiles + n_pairs - 1) / n_pairs;
+    double eff = (double)N_out / (double)(nb * bn) * (double)tiles / (double)(waves * n_pairs);
+    // Fitted to B200 A/B runs (profiles/r01_perf_sweep.log): 256-wide tiles lose ~12 % to the
+    // extra L2->SMEM traffic; 512-wide tiles lose an un-overlapped epilogue of ~4.5 k-blocks per tile.
+    const double kb = (double)((K + kBK - 1) / kBK);
+    eff *= ns == 1 ? 1.0 / 1.12 : kb / (kb + 4.5);
+    if (eff > best) best = eff, pick = ns;
+  }
+  return pick;
 }
 
 tl_status zero_fill(void* out, int64_t n, cudaStream_t s) {
@@ -306,7 +340,9 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   p.M_r = (int)M_r;
   p.epoch = epoch;
   p.m_blocks = (int)((M + 128 * pair - 1) / (128 * pair));
-  p.n_blocks = (int)((N_out + (act ? 128 : 256) - 1) / (act ? 128 : 256));
+  const int nsub = choose_nsub(c, M, N_out, K, act != TL_ACT_NONE);
+  const int bn_out = (act ? 128 : 256) * nsub;
+  p.n_blocks = (int)((N_out + bn_out - 1) / bn_out);
   p.k_blocks = (int)((K + kBK - 1) / kBK);
   p.tm_rows = sm.Tm;
   p.tiles_per_rank = sm.tiles_per_rank;
@@ -343,7 +379,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   }
   if (st == TL_OK) {
     const int epi = act == TL_ACT_NONE ? EPI_STORE : act == TL_ACT_SILU_MUL ? EPI_SILU_MUL : EPI_GELU_MUL;
-    st = launch(c, p, epi, comm, stream);
+    st = launch(c, p, epi, comm, nsub, stream);
   }
   delete pp;
   if (st != TL_OK) return st;
@@ -374,7 +410,8 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
   if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31)) return fail(TL_ERR_UNSUPPORTED, "dimension >= 2^31");
   const int64_t M_r = M / W;
   const int pair = pair_of(c);
-  const int64_t n_blocks = (N + 255) / 256;
+  const int nsub = choose_nsub(c, M, N, K, false);
+  const int64_t n_blocks = (N + 256 * nsub - 1) / (256 * nsub);
   if (W > 1) {
     if (M_r % 128) return fail(TL_ERR_UNSUPPORTED, "GEMM-RS with world > 1 needs (M/world) %% 128 == 0 (M/world=%lld)",
                                (long long)M_r);
@@ -429,7 +466,7 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
     if ((st = cached_tmap(c, &ra.tm_b0, B[i], N, K, pair == 2 ? 128 : 256, 64)) != TL_OK) break;
     if ((st = cached_tmap(c, &ra.tm_c, C[i], comm ? M_r : M, N, 32, 64)) != TL_OK) break;
   }
-  if (st == TL_OK) st = launch(c, p, comm ? EPI_RS : EPI_STORE, false, stream);
+  if (st == TL_OK) st = launch(c, p, comm ? EPI_RS : EPI_STORE, false, nsub, stream);
   delete pp;
   return st;
 }

@@ -36,12 +36,13 @@ def empty(*shape):
 
 
 # ----------------------------------------------------------------------------- W = 1 GEMM core
-@pytest.mark.parametrize("pair", [1, 2])
+@pytest.mark.parametrize("pair,nsub", [(1, 1), (2, 1), (2, 2)])
 @pytest.mark.parametrize("M,N,K", [(256, 256, 64), (1000, 2752, 1376), (384, 520, 4096), (8, 16, 8)])
-def test_gemm_w1_plain(tl, pair, M, N, K):
+def test_gemm_w1_plain(tl, pair, nsub, M, N, K):
     A, Bs = TI.ag_gemm_inputs(M, N, K, 1, seed=M + N)
     c = tl.Comm.single(0, max_M=M, max_H=K)
     c.set_option("cta_pair", pair)
+    c.set_option("n_sub", nsub)
     C = empty(M, N)
     c.ag_gemm(cuda(A[0]), cuda(Bs[0]), C)
     torch.cuda.synchronize()
@@ -49,13 +50,14 @@ def test_gemm_w1_plain(tl, pair, M, N, K):
     assert O.rel_frobenius(f64(C), ref[0]) < TOL
 
 
-@pytest.mark.parametrize("pair", [1, 2])
+@pytest.mark.parametrize("pair,nsub", [(1, 1), (2, 1), (2, 2)])
 @pytest.mark.parametrize("act", [TI.ACT_SILU_MUL, TI.ACT_GELU_TANH_MUL])
 @pytest.mark.parametrize("M,N,K", [(256, 128, 64), (1000, 1376, 520)])
-def test_gemm_w1_gated(tl, pair, act, M, N, K):
+def test_gemm_w1_gated(tl, pair, nsub, act, M, N, K):
     A, Bs = TI.ag_gemm_inputs(M, 2 * N, K, 1, seed=7)
     c = tl.Comm.single(0, max_M=M, max_H=K)
     c.set_option("cta_pair", pair)
+    c.set_option("n_sub", nsub)
     C = empty(M, N)
     c.ag_gemm(cuda(A[0]), cuda(Bs[0]), C, act=act)
     torch.cuda.synchronize()
@@ -115,10 +117,12 @@ def test_ag_gemm_placement_bit_exact(tl, W):
 
 @pytest.mark.parametrize("W", [2, 4, 8])
 @pytest.mark.parametrize("act", [TI.ACT_NONE, TI.ACT_SILU_MUL])
-def test_ag_gemm_random(tl, W, act):
+@pytest.mark.parametrize("nsub", [1, 2])
+def test_ag_gemm_random(tl, W, act, nsub):
     M, K, N = 256 * W, 320, 200 if act else 392
     As, Bs = TI.ag_gemm_inputs(M, (2 if act else 1) * N, K, W, seed=W)
     c = tl.Comm.loopback(W, 0, max_M=M, max_H=K)
+    c.set_option("n_sub", nsub)
     Cs = [empty(M, N) for _ in range(W)]
     c.ag_gemm_lb([cuda(a) for a in As], [cuda(b) for b in Bs], Cs, act=act)
     st, diag = c.check()
@@ -168,11 +172,13 @@ def test_ag_decoupling_soundness(tl):
 # ----------------------------------------------------------------------------- GEMM-RS (loopback W)
 @pytest.mark.parametrize("W", [2, 4, 8])
 @pytest.mark.parametrize("ring", [0, 1])
-def test_gemm_rs_placement_bit_exact(tl, W, ring):
+@pytest.mark.parametrize("nsub", [1, 2])
+def test_gemm_rs_placement_bit_exact(tl, W, ring, nsub):
     M, N, K = 128 * W, 520, 32
     As, Bs = TI.rs_placement_inputs(M, N, K, W)
     c = tl.Comm.loopback(W, 0, max_M=M, max_H=N)
     c.set_option("rs_order", ring)
+    c.set_option("n_sub", nsub)
     Cs = [empty(M // W, N) for _ in range(W)]
     c.gemm_rs_lb([cuda(a) for a in As], [cuda(b) for b in Bs], Cs)
     st, diag = c.check()
@@ -184,11 +190,13 @@ def test_gemm_rs_placement_bit_exact(tl, W, ring):
 
 @pytest.mark.parametrize("W", [2, 4, 8])
 @pytest.mark.parametrize("ring", [0, 1])
-def test_gemm_rs_random(tl, W, ring):
-    M, N, K = 256 * W, 392, 1376 // 4
+@pytest.mark.parametrize("nsub", [1, 2])
+def test_gemm_rs_random(tl, W, ring, nsub):
+    M, N, K = 256 * W, 392 if nsub == 1 else 1032, 1376 // 4
     As, Bs = TI.gemm_rs_inputs(M, N, K, W, seed=3)
     c = tl.Comm.loopback(W, 0, max_M=M, max_H=N)
     c.set_option("rs_order", ring)
+    c.set_option("n_sub", nsub)
     Cs = [empty(M // W, N) for _ in range(W)]
     c.gemm_rs_lb([cuda(a) for a in As], [cuda(b) for b in Bs], Cs)
     st, diag = c.check()
@@ -215,11 +223,12 @@ def test_gemm_rs_deterministic(tl):
 
 
 # ----------------------------------------------------------------------------- MLP (the layer)
-def _mlp_case(tl, W, M, H, I, act, pair=2, seed=0):
+def _mlp_case(tl, W, M, H, I, act, pair=2, seed=0, nsub=0):
     X, G, U, W2 = TI.mlp_full(M, H, I, seed=seed)
     Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, act)
     c = tl.Comm.loopback(W, 0, max_M=M, max_H=H) if W > 1 else tl.Comm.single(0, max_M=M, max_H=H)
     c.set_option("cta_pair", pair)
+    c.set_option("n_sub", nsub)
     outs = [empty(M // W, H) for _ in range(W)]
     if W > 1:
         c.mlp_forward_lb([cuda(x) for x in Xs], [cuda(w) for w in W1s], [cuda(w) for w in W2s], outs, act=act)
@@ -233,10 +242,11 @@ def _mlp_case(tl, W, M, H, I, act, pair=2, seed=0):
 
 @pytest.mark.parametrize("W", [1, 2, 4, 8])
 @pytest.mark.parametrize("act", [TI.ACT_NONE, TI.ACT_SILU_MUL, TI.ACT_GELU_TANH_MUL])
-def test_mlp_tiny_config(tl, W, act):
+@pytest.mark.parametrize("nsub", [1, 2])
+def test_mlp_tiny_config(tl, W, act, nsub):
     """BASELINE.json configs[0]: M=256 tokens, hidden 128, ffn 512 (W=2 in the config; all W here)."""
     M, H, I = 256 * W if W > 2 else 256, 128, 512
-    Xs, W1s, W2s, outs = _mlp_case(tl, W, M, H, I, act)
+    Xs, W1s, W2s, outs = _mlp_case(tl, W, M, H, I, act, nsub=nsub)
     ref = O.mlp_forward([TI.to_f64(x) for x in Xs], [TI.to_f64(w) for w in W1s], [TI.to_f64(w) for w in W2s], act)
     got = np.concatenate([f64(o) for o in outs], 0)
     assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
