@@ -96,20 +96,17 @@ __device__ __forceinline__ void ag_wait_rows(const Params& p, int rank, int lo, 
   }
 }
 
-// Convert 64 fp32 values of this thread's row to bf16, write them into the warp's swizzled
+// Write 64 bf16 values (32 packed words) of this thread's row into the warp's swizzled
 // 32 x 128 B staging buffer and TMA-store the 64 x 32 box at (col, row).
-__device__ __forceinline__ void store_chunk(const float* v, uint8_t* bufs, int& sbuf, const CUtensorMap* tm,
+__device__ __forceinline__ void store_chunk(const uint32_t* pk, uint8_t* bufs, int& sbuf, const CUtensorMap* tm,
                                             int col, int row, uint32_t lane) {
   uint8_t* buf = bufs + sbuf * 4096;
   if (lane == 0) ptx::bulk_wait_read<1>();
   __syncwarp();
   const uint32_t row_addr = ptx::smem_u32(buf) + lane * 128;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    ptx::st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), ptx::pack_bf16x2(v[8 * j + 0], v[8 * j + 1]),
-                      ptx::pack_bf16x2(v[8 * j + 2], v[8 * j + 3]), ptx::pack_bf16x2(v[8 * j + 4], v[8 * j + 5]),
-                      ptx::pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
-  }
+  for (int j = 0; j < 8; ++j)
+    ptx::st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
   ptx::fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
@@ -119,10 +116,10 @@ __device__ __forceinline__ void store_chunk(const float* v, uint8_t* bufs, int& 
   sbuf ^= 1;
 }
 
-// acc[0..63] += bf16 slot row segment (8 x 16 B), columns beyond N skipped (N % 8 == 0).
-__device__ __forceinline__ void add_slot_row(float* acc, const uint16_t* rowp, int col, int N) {
+// acc[0..31] += bf16 slot row segment (4 x 16 B), columns beyond N skipped (N % 8 == 0).
+__device__ __forceinline__ void add_slot32(float* acc, const uint16_t* rowp, int col, int N) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < 4; ++j) {
     if (col + 8 * j < N) {
       const uint4 q = ptx::ld_global_v4(rowp + col + 8 * j);
       const uint32_t w[4] = {q.x, q.y, q.z, q.w};
@@ -135,9 +132,34 @@ __device__ __forceinline__ void add_slot_row(float* acc, const uint16_t* rowp, i
   }
 }
 
-__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// SiLU(g) = g * sigmoid(g) = h + h * tanh(h) with h = g/2: one MUFU op per element.
+__device__ __forceinline__ float silu_f(float g) {
+  const float h = 0.5f * g;
+  return fmaf(h, tanh_approx(h), h);
+}
+// GeLU (tanh approximation) = h + h * tanh(sqrt(2/pi) (g + 0.044715 g^3)), h = g/2.
 __device__ __forceinline__ float gelu_tanh_f(float g) {
-  return 0.5f * g * (1.0f + tanhf(0.7978845608028654f * (g + 0.044715f * g * g * g)));
+  const float h = 0.5f * g;
+  const float in = 0.7978845608028654f * g * fmaf(0.044715f * g, g, 1.0f);
+  return fmaf(h, tanh_approx(in), h);
+}
+
+// Epilogue piece = 32 output columns of this warp's 32 rows.  Plain/RS: accumulator columns
+// [32 pc, 32 pc + 32); gated: gate columns and the matching up columns (+128) of sub-tile pc/4.
+template <bool kGated>
+__device__ __forceinline__ void epi_load(uint32_t tacc, int pc, float* r) {
+  if constexpr (kGated) {
+    const uint32_t tg = tacc + (pc >> 2) * kUmmaN + (pc & 3) * 32;
+    ptx::tmem_ld32(tg, r);
+    ptx::tmem_ld32(tg + 128, r + 32);
+  } else {
+    ptx::tmem_ld32(tacc + pc * 32, r);
+  }
 }
 
 template <int kPair, int kStages, int kEpi, bool kAG, int kNSub>
@@ -325,102 +347,104 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(&tempty[as], 0);
       };
-      float v[64];
-      if constexpr (kEpi == EPI_STORE) {
-#pragma unroll 1
-        for (int c = 0; c < 4 * kNSub; ++c) {
-          ptx::tmem_ld32(tacc + c * 64, v);
-          ptx::tmem_ld32(tacc + c * 64 + 32, v + 32);
-          ptx::tmem_ld_wait();
-          if (c == 4 * kNSub - 1) release_tmem();
-          store_chunk(v, bufs, sbuf, &ra.tm_c, nb * kAccCols + c * 64, row0 + ew * 32, lane);
+      // ---- per-tile action: plain/gated store, or (GEMM-RS) push to a peer slot / own reduce
+      constexpr bool kGated = (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL);
+      constexpr int kPieces = (kGated ? 4 : 8) * kNSub;       // 32-column output pieces
+      constexpr int kPW = kGated ? 64 : 32;                   // fp32 registers per loaded piece
+      const int out_col0 = nb * (kGated ? 128 : 256) * kNSub;
+      const CUtensorMap* tm_out = &ra.tm_c;
+      int out_row = row0 + ew * 32;
+      bool push = false;
+      int tgt = 0, slot = 0, tile = 0, myrow = 0;
+      uint32_t add_mask = 0;                                   // slots to add (ascending rank order)
+      const uint16_t* stg = nullptr;
+      if constexpr (kEpi == EPI_RS) {
+        if (row0 >= p.M) {                                     // half-tile past the last row
+          release_tmem();
+          continue;
         }
-      } else if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) {
-#pragma unroll 1
-        for (int c = 0; c < 2 * kNSub; ++c) {
-          // sub-tile c/2: accumulator columns [0,128) = gate (leader CTA's B half), [128,256) = up
-          const uint32_t tg = tacc + (c >> 1) * kUmmaN + (c & 1) * 64;
-          float u[64];
-          ptx::tmem_ld32(tg, v);
-          ptx::tmem_ld32(tg + 32, v + 32);
-          ptx::tmem_ld32(tg + 128, u);
-          ptx::tmem_ld32(tg + 128 + 32, u + 32);
-          ptx::tmem_ld_wait();
-          if (c == 2 * kNSub - 1) release_tmem();
-#pragma unroll
-          for (int i = 0; i < 64; ++i)
-            v[i] = (kEpi == EPI_SILU_MUL ? silu_f(v[i]) : gelu_tanh_f(v[i])) * u[i];
-          store_chunk(v, bufs, sbuf, &ra.tm_c, nb * 128 * kNSub + c * 64, row0 + ew * 32, lane);
-        }
-      } else if (row0 >= p.M) {
-        release_tmem();                              // half-tile past the last row: nothing to do
-      } else {
-        // ---------------- GEMM-RS epilogue ----------------
         const int W = p.world;
         const int o = row0 / p.M_r;                 // owner of these rows (offset in the global view)
         const int lrow0 = row0 - o * p.M_r;         // first row inside the owner's block
-        const int tile = (lrow0 / 128) * p.n_blocks + nb;
-        const int myrow = lrow0 + ew * 32 + (int)lane;
-        const uint16_t* stg = p.staging[rank];
-        bool push;
-        int tgt = 0, slot = 0;                       // push target rank and slot
+        tile = (lrow0 / 128) * p.n_blocks + nb;
+        myrow = lrow0 + ew * 32 + (int)lane;
+        stg = p.staging[rank];
         if (p.rs_mode == RS_RING) {
           const int step = (o - rank - 1 + 2 * W) % W;   // o = r+1 -> 0, ..., o = r -> W-1
-          if (step > 0) {                            // peer_tile_wait on the partial from rank r+1
+          if (step > 0) {                                // peer_tile_wait on the partial from rank r+1
             if (lane == 0)
               tile_wait(p.rs_flags[rank] + o * kRsFlagStride + tile, p.epoch, p.timeout_ns, p.diag, rank, 2,
                         (rank + 1) % W, tile);
             __syncwarp();
+            add_mask = 1u << o;
           }
           push = step < W - 1;
           tgt = (rank - 1 + W) % W;
           slot = o;
-#pragma unroll 1
-          for (int c = 0; c < 4 * kNSub; ++c) {
-            ptx::tmem_ld32(tacc + c * 64, v);
-            ptx::tmem_ld32(tacc + c * 64 + 32, v + 32);
-            ptx::tmem_ld_wait();
-            if (c == 4 * kNSub - 1) release_tmem();
-            const int col = nb * kAccCols + c * 64;
-            if (step > 0) add_slot_row(v, stg + ((size_t)o * p.M_r + myrow) * p.N_out, col, p.N_out);
-            if (push)
-              store_chunk(v, bufs, sbuf, &p.tm_stage[tgt], col, slot * p.M_r + lrow0 + ew * 32, lane);
-            else
-              store_chunk(v, bufs, sbuf, &ra.tm_c, col, lrow0 + ew * 32, lane);
-          }
         } else {
           push = o != rank;
           tgt = o;
           slot = rank;
-          if (!push) {                               // owner: peer_tile_wait on every other slot
+          if (!push) {                                   // owner: peer_tile_wait on every other slot
             if ((int)lane < W && (int)lane != rank)
               tile_wait(p.rs_flags[rank] + lane * kRsFlagStride + tile, p.epoch, p.timeout_ns, p.diag, rank, 2,
                         lane, tile);
             __syncwarp();
-          }
-#pragma unroll 1
-          for (int c = 0; c < 4 * kNSub; ++c) {
-            ptx::tmem_ld32(tacc + c * 64, v);
-            ptx::tmem_ld32(tacc + c * 64 + 32, v + 32);
-            ptx::tmem_ld_wait();
-            if (c == 4 * kNSub - 1) release_tmem();
-            const int col = nb * kAccCols + c * 64;
-            if (push) {
-              store_chunk(v, bufs, sbuf, &p.tm_stage[tgt], col, slot * p.M_r + lrow0 + ew * 32, lane);
-            } else {
-              for (int s = 0; s < W; ++s)            // own fp32 partial + slots, ascending rank
-                if (s != rank) add_slot_row(v, stg + ((size_t)s * p.M_r + myrow) * p.N_out, col, p.N_out);
-              store_chunk(v, bufs, sbuf, &ra.tm_c, col, lrow0 + ew * 32, lane);
-            }
+            add_mask = ((1u << W) - 1) & ~(1u << rank);
           }
         }
+        if (push) {
+          tm_out = &p.tm_stage[tgt];
+          out_row = slot * p.M_r + lrow0 + ew * 32;
+        } else {
+          out_row = lrow0 + ew * 32;
+        }
+      }
+      // piece -> 16 packed bf16x2 words (activation / slot reduction in fp32)
+      auto compute = [&](float* r, int pc, uint32_t* out16) {
+        if constexpr (kGated) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a0 = (kEpi == EPI_SILU_MUL ? silu_f(r[2 * i]) : gelu_tanh_f(r[2 * i])) * r[32 + 2 * i];
+            const float a1 =
+                (kEpi == EPI_SILU_MUL ? silu_f(r[2 * i + 1]) : gelu_tanh_f(r[2 * i + 1])) * r[32 + 2 * i + 1];
+            out16[i] = ptx::pack_bf16x2(a0, a1);
+          }
+        } else {
+          if constexpr (kEpi == EPI_RS) {
+            if (add_mask) {
+              const int col = out_col0 + pc * 32;
+              for (int s2 = 0; s2 < p.world; ++s2)       // own fp32 partial + slots, ascending rank
+                if (add_mask & (1u << s2)) add_slot32(r, stg + ((size_t)s2 * p.M_r + myrow) * p.N_out, col, p.N_out);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) out16[i] = ptx::pack_bf16x2(r[2 * i], r[2 * i + 1]);
+        }
+      };
+      // ---- software pipeline: TMEM loads of piece p+1 overlap the math and stores of piece p
+      float ra_[kPW], rb_[kPW];
+      uint32_t pk[32];
+      epi_load<kGated>(tacc, 0, ra_);
+      ptx::tmem_ld_wait_fence<kPW>(ra_);
+#pragma unroll 1
+      for (int pc = 0; pc < kPieces; pc += 2) {
+        epi_load<kGated>(tacc, pc + 1, rb_);
+        compute(ra_, pc, pk);
+        ptx::tmem_ld_wait_fence<kPW>(rb_);
+        if (pc + 2 == kPieces) release_tmem();
+        else epi_load<kGated>(tacc, pc + 2, ra_);
+        compute(rb_, pc + 1, pk + 16);
+        store_chunk(pk, bufs, sbuf, tm_out, out_col0 + pc * 32, out_row, lane);
+        if (pc + 2 < kPieces) ptx::tmem_ld_wait_fence<kPW>(ra_);
+      }
+      if constexpr (kEpi == EPI_RS) {
         if (push) {
           // every byte of this half-tile has landed in the target's slot -> notify (release)
           if (lane == 0) ptx::bulk_wait<0>();
           __syncwarp();
           ptx::named_bar_sync(1, 128);
-          if (ew == 0 && lane == 0)
-            tile_notify(p.rs_flags[tgt] + slot * kRsFlagStride + tile, p.epoch);
+          if (ew == 0 && lane == 0) tile_notify(p.rs_flags[tgt] + slot * kRsFlagStride + tile, p.epoch);
         }
       }
     }

@@ -228,6 +228,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Wait for outstanding tcgen05.ld, then "touch" the N destination registers in an empty volatile
+// asm ordered after the wait, so no use of them can be scheduled above the wait.
+template <int N>
+__device__ __forceinline__ void tmem_ld_wait_fence(float* r) {
+  tmem_ld_wait();
+#pragma unroll
+  for (int b = 0; b < N; b += 32) {
+    float* q = r + b;
+    asm volatile("" : "+f"(q[0]), "+f"(q[1]), "+f"(q[2]), "+f"(q[3]), "+f"(q[4]), "+f"(q[5]), "+f"(q[6]), "+f"(q[7]), "+f"(q[8]), "+f"(q[9]), "+f"(q[10]), "+f"(q[11]), "+f"(q[12]), "+f"(q[13]), "+f"(q[14]), "+f"(q[15]), "+f"(q[16]), "+f"(q[17]), "+f"(q[18]), "+f"(q[19]), "+f"(q[20]), "+f"(q[21]), "+f"(q[22]), "+f"(q[23]), "+f"(q[24]), "+f"(q[25]), "+f"(q[26]), "+f"(q[27]), "+f"(q[28]), "+f"(q[29]), "+f"(q[30]), "+f"(q[31]) :: "memory");
+  }
+}
 
 // Shared-memory matrix descriptor for a K-major, 128B-swizzled operand tile whose rows are
 // 128 bytes (64 bf16 of K) and whose 8-row swizzle atoms are 1024 bytes apart.
