@@ -270,27 +270,22 @@ def main():
                                                                 np.stack([ref[i] for i in rows])),
                   "tol": 5e-3, "status": int(st)}
 
-    # ---- end to end through the public API: pinned host X in, host out back, every step
-    x_host = Xs[rank].pin_memory()
-    out_host = torch.empty(Mr, HID, dtype=torch.bfloat16).pin_memory()
-    xin = torch.empty_like(x)
-
-    def e2e_step():
-        xin.copy_(x_host, non_blocking=True)
-        comm.mlp_forward(xin, w1, w2, out, act=tl.ACT_SILU_MUL, Z=Z, stream=stream)
-        out_host.copy_(out, non_blocking=True)
-
-    for _ in range(2):
-        e2e_step()
+    # ---- end to end through the public API: every step copies its X shard in from pinned host
+    # memory and its output back to pinned host memory (paper_2503_20313_b200.pipeline.MLPPipeline:
+    # H2D of step i+1 and D2H of step i-1 overlap the layer of step i on separate streams)
+    from paper_2503_20313_b200.pipeline import MLPPipeline
+    pipe = MLPPipeline(comm, w1, w2, tl.ACT_SILU_MUL, Mr, HID)
+    hx = [Xs[rank].pin_memory(), (Xs[rank].float() * -1.0).to(torch.bfloat16).pin_memory()]
+    hin = [hx[i % 2] for i in range(args.steps)]
+    hout = [torch.empty(Mr, HID, dtype=torch.bfloat16).pin_memory() for _ in range(args.steps)]
+    pipe.run(hin[:2], hout[:2])
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    e1.record(stream)
+    pipe.run(hin, hout, e0, e1)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
     e2e_val = (f1 + f2) * W / (e2e_ms * 1e-3) / 1e12
+    e2e_match = bool(torch.equal(hout[0], out.cpu()))   # same input as the device-resident run, bitwise
 
     # ---- non-overlapped NCCL + cuBLAS baseline (same inputs, same protocol)
     base = None
@@ -385,8 +380,10 @@ def main():
                      "per_launch_flop": f1},
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_val, 2), "unit": "TFLOPS", "ms_per_step": round(e2e_ms, 4),
-                "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": out.numel() * 2,
-                "api": "tl_mlp_forward via paper_2503_20313_b200.Comm.mlp_forward, pinned host X in / out back"},
+                "h2d_bytes_per_step": pipe.bytes_in, "d2h_bytes_per_step": pipe.bytes_out,
+                "api": "tl_mlp_forward via paper_2503_20313_b200.pipeline.MLPPipeline (pinned host X shard in, "
+                       "output back, every step; copies overlap the previous/next step's layer)",
+                "output_matches_device_run": e2e_match},
         "gpu_launches": 2 * args.steps,
         "clocks": clk,
         "parity": parity,

@@ -245,28 +245,39 @@ tl_status launch(tl_comm* c, const Params& p, int epi, bool ag, int nsub, cudaSt
   return launch_t<1, EPI_RS, false, 1>(c, p, s);
 }
 
-// Number of 256-column MMA sub-tiles per tile (option n_sub, 0 = auto): 512-wide tiles move 25 %
-// fewer bytes per FLOP but quantise N and the wave count more coarsely and serialise the epilogue.
+// Split point of the work list: with 512-wide tiles a last wave that is at most half full is run
+// as 256-wide half items (half the time), every other tile whole.
+void set_items(Params& p, int nsub, int n_pairs) {
+  const int T = p.m_blocks * p.n_blocks;
+  const int rem = T % n_pairs;
+  if (nsub == 2 && rem != 0 && 2 * rem <= n_pairs) {
+    p.n_full = T - rem;
+    p.n_items = p.n_full + 2 * rem;
+  } else {
+    p.n_full = T;
+    p.n_items = T;
+  }
+}
+
+// Number of 256-column MMA sub-tiles per tile (option n_sub, 0 = auto), from a time model fitted
+// to B200 A/B runs (profiles/r01_perf_sweep*.log), in units of one 256-wide k-block of MMAs:
+// 256-wide tiles (TMEM double-buffered, epilogue hidden) cost 1.12 per k-block (extra L2->SMEM
+// traffic); 512-wide tiles cost 2 per k-block plus ~9 for the un-overlapped epilogue; half items
+// (split tail) cost 1 per k-block plus ~4.5.
 int choose_nsub(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gated) {
   if (pair_of(c) != 2) return 1;
   if (c->opt.n_sub == 1 || c->opt.n_sub == 2) return (int)c->opt.n_sub;
-  const int n_pairs = ctas_per_rank(c) / 2;
+  const int64_t P = ctas_per_rank(c) / 2;
   const int64_t m_blocks = (M + 255) / 256;
-  double best = -1;
-  int pick = 1;
-  for (int ns = 1; ns <= 2; ++ns) {
-    const int64_t bn = (gated ? 128 : 256) * ns;
-    const int64_t nb = (N_out + bn - 1) / bn;
-    const int64_t tiles = m_blocks * nb;
-    const int64_t waves = (tiles + n_pairs - 1) / n_pairs;
-    double eff = (double)N_out / (double)(nb * bn) * (double)tiles / (double)(waves * n_pairs);
-    // Fitted to B200 A/B runs (profiles/r01_perf_sweep.log): 256-wide tiles lose ~12 % to the
-    // extra L2->SMEM traffic; 512-wide tiles lose an un-overlapped epilogue of ~4.5 k-blocks per tile.
-    const double kb = (double)((K + kBK - 1) / kBK);
-    eff *= ns == 1 ? 1.0 / 1.12 : kb / (kb + 4.5);
-    if (eff > best) best = eff, pick = ns;
-  }
-  return pick;
+  const double kb = (double)((K + kBK - 1) / kBK);
+  const int64_t bn1 = gated ? 128 : 256;
+  const int64_t T1 = m_blocks * ((N_out + bn1 - 1) / bn1);
+  const int64_t T2 = m_blocks * ((N_out + 2 * bn1 - 1) / (2 * bn1));
+  const double t1 = (double)((T1 + P - 1) / P) * 1.12 * kb;
+  const int64_t rem = T2 % P;
+  const double full2 = 2.0 * kb + 9.0;
+  const double t2 = (double)(T2 / P) * full2 + (rem == 0 ? 0.0 : (2 * rem <= P ? kb + 4.5 : full2));
+  return t2 < t1 ? 2 : 1;
 }
 
 tl_status zero_fill(void* out, int64_t n, cudaStream_t s) {
@@ -344,6 +355,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   const int bn_out = (act ? 128 : 256) * nsub;
   p.n_blocks = (int)((N_out + bn_out - 1) / bn_out);
   p.k_blocks = (int)((K + kBK - 1) / kBK);
+  set_items(p, nsub, p.ctas_per_rank / pair);
   p.tm_rows = sm.Tm;
   p.tiles_per_rank = sm.tiles_per_rank;
   p.tiles_per_channel = sm.tiles_per_channel;
@@ -415,7 +427,8 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
   if (W > 1) {
     if (M_r % 128) return fail(TL_ERR_UNSUPPORTED, "GEMM-RS with world > 1 needs (M/world) %% 128 == 0 (M/world=%lld)",
                                (long long)M_r);
-    if ((M_r / 128) * n_blocks > kRsFlagStride) return fail(TL_ERR_UNSUPPORTED, "too many RS tiles per owner block");
+    if ((M_r / 128) * n_blocks * nsub > kRsFlagStride)
+      return fail(TL_ERR_UNSUPPORTED, "too many RS tiles per owner block");
   }
   for (int i = 0; i < c->n_local; ++i) {
     if ((!A[i] && M * K) || (!B[i] && N * K) || (!C[i] && M_r * N))
@@ -443,6 +456,7 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
   p.m_blocks = (int)((M + 128 * pair - 1) / (128 * pair));
   p.n_blocks = (int)n_blocks;
   p.k_blocks = (int)((K + kBK - 1) / kBK);
+  set_items(p, nsub, p.ctas_per_rank / pair);
   p.rs_mode = comm ? (c->opt.rs_order == 1 ? RS_RING : RS_ONESHOT) : RS_NONE;
   p.order = comm ? ORDER_ROTATE : ORDER_IDENTITY;
   p.tm_rows = 1;

@@ -17,6 +17,8 @@
 // Communication tile (Tm_p rows) and compute tile (128*kPair x 256) are chosen independently
 // (the decoupled design space).
 #pragma once
+#include <type_traits>
+
 #include "tl_params.h"
 #include "tl_primitives.cuh"
 #include "tl_ptx.cuh"
@@ -79,6 +81,21 @@ __device__ __forceinline__ void tile_coords(const Params& p, int rank, int m_rot
   const int local = t - group * per_group;
   nb = local / rows;
   mb = m_perm(p, rank, m_rot, first + local % rows);
+}
+
+// Work item -> tile and the range of 256-column sub-tiles it computes.
+template <int kNSub>
+__device__ __forceinline__ void item_coords(const Params& p, int item, int& t, int& sub_lo, int& sub_n) {
+  if (kNSub == 1 || item < p.n_full) {
+    t = item;
+    sub_lo = 0;
+    sub_n = kNSub;
+  } else {
+    const int j = item - p.n_full;
+    t = p.n_full + j / kNSub;
+    sub_lo = j % kNSub;
+    sub_n = 1;
+  }
 }
 
 // consumer_tile_wait for A rows [lo, hi) of the gathered tensor: every producer tile of every
@@ -177,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
   const int pair = cta_in_rank / kPair, n_pairs = p.ctas_per_rank / kPair;
   const RankArgs& ra = p.rk[lr];
   const int rank = ra.rank;
-  const int total = p.m_blocks * p.n_blocks;
+  const int total = p.n_items;
   constexpr int BM = 128 * kPair;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::off_bar);
@@ -217,44 +234,52 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < total; t += n_pairs) {
-        int mb, nb;
+      for (int item = pair; item < total; item += n_pairs) {
+        int t, sub_lo, sub_n, mb, nb;
+        item_coords<kNSub>(p, item, t, sub_lo, sub_n);
         tile_coords(p, rank, ra.m_rot, t, mb, nb);
         const int row0 = mb * BM + cta_in_pair * 128;
         if constexpr (kAG) {
           if (row0 < p.M) ag_wait_rows(p, rank, row0, min(row0 + 128, p.M));
         }
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + L::off_a + stage * kAStage;
-          uint8_t* sb = smem + L::off_b + stage * L::kBStage;
-          const int kc = kb * kBK;
-          if constexpr (kPair == 2) {
-            ptx::tma_load_2d_pair(&ra.tm_a, &full[stage], sa, kc, row0);
+        // the sub-tile count is a compile-time constant inside the k-loop (hoisted branch)
+        auto produce = [&](auto ns_c, int s_lo) {
+          constexpr int NS = decltype(ns_c)::value;
+          for (int kb = 0; kb < p.k_blocks; ++kb) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + L::off_a + stage * kAStage;
+            uint8_t* sb = smem + L::off_b + stage * L::kBStage;
+            const int kc = kb * kBK;
+            if constexpr (kPair == 2) {
+              ptx::tma_load_2d_pair(&ra.tm_a, &full[stage], sa, kc, row0);
 #pragma unroll
-            for (int sub = 0; sub < kNSub; ++sub) {
-              if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL)
-                ptx::tma_load_2d_pair(cta_in_pair == 0 ? &ra.tm_b0 : &ra.tm_b1, &full[stage], sb + sub * L::kBBox,
-                                      kc, nb * 128 * kNSub + sub * 128);
-              else
-                ptx::tma_load_2d_pair(&ra.tm_b0, &full[stage], sb + sub * L::kBBox, kc,
-                                      nb * kAccCols + sub * kUmmaN + cta_in_pair * 128);
-            }
-          } else {
-            ptx::tma_load_2d(&ra.tm_a, &full[stage], sa, kc, row0);
-            if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) {
-              ptx::tma_load_2d(&ra.tm_b0, &full[stage], sb, kc, nb * 128);
-              ptx::tma_load_2d(&ra.tm_b1, &full[stage], sb + 128 * 128, kc, nb * 128);
+              for (int q = 0; q < NS; ++q) {
+                const int sub = s_lo + q;
+                if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL)
+                  ptx::tma_load_2d_pair(cta_in_pair == 0 ? &ra.tm_b0 : &ra.tm_b1, &full[stage], sb + sub * L::kBBox,
+                                        kc, nb * 128 * kNSub + sub * 128);
+                else
+                  ptx::tma_load_2d_pair(&ra.tm_b0, &full[stage], sb + sub * L::kBBox, kc,
+                                        nb * kAccCols + sub * kUmmaN + cta_in_pair * 128);
+              }
             } else {
-              ptx::tma_load_2d(&ra.tm_b0, &full[stage], sb, kc, nb * kUmmaN);
+              ptx::tma_load_2d(&ra.tm_a, &full[stage], sa, kc, row0);
+              if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) {
+                ptx::tma_load_2d(&ra.tm_b0, &full[stage], sb, kc, nb * 128);
+                ptx::tma_load_2d(&ra.tm_b1, &full[stage], sb + 128 * 128, kc, nb * 128);
+              } else {
+                ptx::tma_load_2d(&ra.tm_b0, &full[stage], sb, kc, nb * kUmmaN);
+              }
             }
+            if (cta_in_pair == 0)
+              ptx::mbar_arrive_expect_tx(&full[stage], (kAStage + NS * L::kBBox) * kPair);
+            else
+              ptx::mbar_arrive_cluster(&full[stage], 0);
+            if (++stage == kStages) stage = 0, phase ^= 1;
           }
-          if (cta_in_pair == 0)
-            ptx::mbar_arrive_expect_tx(&full[stage], (kAStage + L::kBStage) * kPair);
-          else
-            ptx::mbar_arrive_cluster(&full[stage], 0);
-          if (++stage == kStages) stage = 0, phase ^= 1;
-        }
+        };
+        if (sub_n == kNSub) produce(std::integral_constant<int, kNSub>{}, 0);
+        else produce(std::integral_constant<int, 1>{}, sub_lo);
       }
     }
   } else if (warp == 1) {
@@ -263,29 +288,38 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       constexpr uint32_t idesc = ptx::idesc_bf16(128 * kPair, kUmmaN);
       int stage = 0, it = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < total; t += n_pairs, ++it) {
+      for (int item = pair; item < total; item += n_pairs, ++it) {
+        int t, sub_lo, sub_n;
+        item_coords<kNSub>(p, item, t, sub_lo, sub_n);
         const int as = it % kAccBufs;
         ptx::mbar_wait(&tempty[as], ((it / kAccBufs) & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t tmem_d = tmem_base + as * kAccCols;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
-          ptx::tc_fence_after();
-          if (lane == 0) {
-            const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(smem + L::off_a + stage * kAStage));
-            const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(smem + L::off_b + stage * L::kBStage));
+        auto issue = [&](auto ns_c, int s_lo) {
+          constexpr int NS = decltype(ns_c)::value;
+          for (int kb = 0; kb < p.k_blocks; ++kb) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            if (lane == 0) {
+              const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(smem + L::off_a + stage * kAStage));
+              const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(smem + L::off_b + stage * L::kBStage)) +
+                                  s_lo * (L::kBBox >> 4);
+              const uint32_t td = tmem_d + s_lo * kUmmaN;
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
+              for (int k = 0; k < kBK / 16; ++k)
 #pragma unroll
-              for (int sub = 0; sub < kNSub; ++sub)
-                ptx::mma_bf16<kPair>(ad + 2 * k, bd + sub * (L::kBBox >> 4) + 2 * k, tmem_d + sub * kUmmaN, idesc,
-                                     (kb | k) != 0);
-            ptx::mma_commit<kPair>(&empty[stage]);
-            if (kb == p.k_blocks - 1) ptx::mma_commit<kPair>(&tfull[as]);
+                for (int q = 0; q < NS; ++q)
+                  ptx::mma_bf16<kPair>(ad + 2 * k, bd + q * (L::kBBox >> 4) + 2 * k, td + q * kUmmaN, idesc,
+                                       (kb | k) != 0);
+              ptx::mma_commit<kPair>(&empty[stage]);
+              if (kb == p.k_blocks - 1) ptx::mma_commit<kPair>(&tfull[as]);
+            }
+            __syncwarp();
+            if (++stage == kStages) stage = 0, phase ^= 1;
           }
-          __syncwarp();
-          if (++stage == kStages) stage = 0, phase ^= 1;
-        }
+        };
+        if (sub_n == kNSub) issue(std::integral_constant<int, kNSub>{}, 0);
+        else issue(std::integral_constant<int, 1>{}, sub_lo);
       }
     }
   } else if (warp == 3) {
@@ -334,8 +368,9 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     const int ew = warp - 4;
     uint8_t* bufs = smem + L::off_epi + ew * 8192;
     int sbuf = 0, it = 0;
-    for (int t = pair; t < total; t += n_pairs, ++it) {
-      int mb, nb;
+    for (int item = pair; item < total; item += n_pairs, ++it) {
+      int t, sub_lo, sub_n, mb, nb;
+      item_coords<kNSub>(p, item, t, sub_lo, sub_n);
       tile_coords(p, rank, ra.m_rot, t, mb, nb);
       const int as = it % kAccBufs;
       ptx::mbar_wait(&tfull[as], (it / kAccBufs) & 1);
@@ -349,7 +384,8 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       };
       // ---- per-tile action: plain/gated store, or (GEMM-RS) push to a peer slot / own reduce
       constexpr bool kGated = (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL);
-      constexpr int kPieces = (kGated ? 4 : 8) * kNSub;       // 32-column output pieces
+      constexpr int kPPS = kGated ? 4 : 8;                     // 32-column output pieces per sub-tile
+      const int pc0 = sub_lo * kPPS, pc_end = (sub_lo + sub_n) * kPPS;
       constexpr int kPW = kGated ? 64 : 32;                   // fp32 registers per loaded piece
       const int out_col0 = nb * (kGated ? 128 : 256) * kNSub;
       const CUtensorMap* tm_out = &ra.tm_c;
@@ -366,15 +402,15 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         const int W = p.world;
         const int o = row0 / p.M_r;                 // owner of these rows (offset in the global view)
         const int lrow0 = row0 - o * p.M_r;         // first row inside the owner's block
-        tile = (lrow0 / 128) * p.n_blocks + nb;
+        tile = (lrow0 / 128) * (p.n_blocks * kNSub) + nb * kNSub + sub_lo;   // flag per 128 x 256 sub-tile
         myrow = lrow0 + ew * 32 + (int)lane;
         stg = p.staging[rank];
         if (p.rs_mode == RS_RING) {
           const int step = (o - rank - 1 + 2 * W) % W;   // o = r+1 -> 0, ..., o = r -> W-1
           if (step > 0) {                                // peer_tile_wait on the partial from rank r+1
-            if (lane == 0)
-              tile_wait(p.rs_flags[rank] + o * kRsFlagStride + tile, p.epoch, p.timeout_ns, p.diag, rank, 2,
-                        (rank + 1) % W, tile);
+            if ((int)lane < sub_n)
+              tile_wait(p.rs_flags[rank] + o * kRsFlagStride + tile + lane, p.epoch, p.timeout_ns, p.diag, rank, 2,
+                        (rank + 1) % W, tile + lane);
             __syncwarp();
             add_mask = 1u << o;
           }
@@ -386,9 +422,10 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
           tgt = o;
           slot = rank;
           if (!push) {                                   // owner: peer_tile_wait on every other slot
-            if ((int)lane < W && (int)lane != rank)
-              tile_wait(p.rs_flags[rank] + lane * kRsFlagStride + tile, p.epoch, p.timeout_ns, p.diag, rank, 2,
-                        lane, tile);
+            for (int q = 0; q < sub_n; ++q)
+              if ((int)lane < W && (int)lane != rank)
+                tile_wait(p.rs_flags[rank] + lane * kRsFlagStride + tile + q, p.epoch, p.timeout_ns, p.diag, rank,
+                          2, lane, tile + q);
             __syncwarp();
             add_mask = ((1u << W) - 1) & ~(1u << rank);
           }
@@ -425,18 +462,18 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       // ---- software pipeline: TMEM loads of piece p+1 overlap the math and stores of piece p
       float ra_[kPW], rb_[kPW];
       uint32_t pk[32];
-      epi_load<kGated>(tacc, 0, ra_);
+      epi_load<kGated>(tacc, pc0, ra_);
       ptx::tmem_ld_wait_fence<kPW>(ra_);
 #pragma unroll 1
-      for (int pc = 0; pc < kPieces; pc += 2) {
+      for (int pc = pc0; pc < pc_end; pc += 2) {
         epi_load<kGated>(tacc, pc + 1, rb_);
         compute(ra_, pc, pk);
         ptx::tmem_ld_wait_fence<kPW>(rb_);
-        if (pc + 2 == kPieces) release_tmem();
+        if (pc + 2 == pc_end) release_tmem();
         else epi_load<kGated>(tacc, pc + 2, ra_);
         compute(rb_, pc + 1, pk + 16);
         store_chunk(pk, bufs, sbuf, tm_out, out_col0 + pc * 32, out_row, lane);
-        if (pc + 2 < kPieces) ptx::tmem_ld_wait_fence<kPW>(ra_);
+        if (pc + 2 < pc_end) ptx::tmem_ld_wait_fence<kPW>(ra_);
       }
       if constexpr (kEpi == EPI_RS) {
         if (push) {
@@ -444,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
           if (lane == 0) ptx::bulk_wait<0>();
           __syncwarp();
           ptx::named_bar_sync(1, 128);
-          if (ew == 0 && lane == 0) tile_notify(p.rs_flags[tgt] + slot * kRsFlagStride + tile, p.epoch);
+          if (ew == 0 && (int)lane < sub_n) tile_notify(p.rs_flags[tgt] + slot * kRsFlagStride + tile + lane, p.epoch);
         }
       }
     }

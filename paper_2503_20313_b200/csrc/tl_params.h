@@ -39,6 +39,9 @@ struct alignas(64) Params {
   uint64_t timeout_ns;
   int M, N_out, K, M_r, world, n_local, ctas_per_rank;
   int m_blocks, n_blocks, k_blocks, raster_group, order;
+  // work items: tiles [0, n_full) run whole; the remaining tiles are split into one item per
+  // 256-column sub-tile (half-width tail when kNSub = 2 and the last wave is at most half full)
+  int n_full, n_items;
   uint32_t epoch;
   // AG (producer = copy role, consumer = GEMM A loads)
   int tm_rows, tiles_per_rank, tiles_per_channel, copy_ctas, row_bytes;

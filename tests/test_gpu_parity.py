@@ -332,3 +332,18 @@ def test_device_static_map_matches_paper_formula(tl, M, R, C, Tm):
     for t in range(n):
         lo, hi = O.static_shape_range(t, M, Tm)
         assert dev[t] == (lo, hi, O.static_src_rank(t, M, R, Tm), O.static_channel(t, M, R, C, Tm))
+
+
+@pytest.mark.parametrize("act", [TI.ACT_NONE, TI.ACT_SILU_MUL])
+def test_split_tail_items(tl, act):
+    """512-wide tiles whose last wave is at most half full run as 256-wide half items
+    (M=8192, N=4096 -> 256 tiles on 74 pairs: 222 whole tiles + 68 half items)."""
+    M, N, K = 8192, 4096 if act == TI.ACT_NONE else 2048, 256
+    A, Bs = TI.ag_gemm_inputs(M, (2 if act else 1) * N, K, 1, seed=21)
+    c = tl.Comm.single(0, max_M=M, max_H=K)
+    c.set_option("n_sub", 2)
+    C = empty(M, N)
+    c.ag_gemm(cuda(A[0]), cuda(Bs[0]), C, act=act)
+    torch.cuda.synchronize()
+    _, Y = O.ag_gemm([TI.to_f64(A[0])], [TI.to_f64(Bs[0])])
+    assert O.rel_frobenius(f64(C), O.activation(Y[0], act)) < TOL
