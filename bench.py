@@ -40,6 +40,14 @@ def layer_flops(M, H, I, W, gated=True):
     return 2 * M * H * (2 * il if gated else il), 2 * M * il * H
 
 
+def bench_config(W):
+    """The workload description shared by both arms (identical `config` in both JSON lines)."""
+    il = FFN // W
+    return {"workload": f"llama7b_mlp_w{W}", "M": M_TOK, "H": HID, "I": FFN, "world": W, "act": "silu_mul",
+            "gemm1": f"[{M_TOK}x{HID}] x [{2 * il}x{HID}]^T", "gemm2": f"[{M_TOK}x{il}] x [{HID}x{il}]^T",
+            "parallelism": f"tp{W}", "l2": "inputs larger than L2 (W1 180 MB + W2 90 MB + X 64 MB > 126 MB)"}
+
+
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -128,8 +136,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(tflops, 6), "unit": "TFLOPS", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"llama7b_mlp_w{W}", "M": M_TOK, "H": HID, "I": FFN, "world": W, "act": "silu_mul",
-                   "sample_rows_per_step": rows_per_step},
+        "config": bench_config(W),
         "cpu_baseline": {"value": round(tflops, 6), "unit": "TFLOPS", "cores": cores, "kind": "oracle",
                          "sample": f"{rows_per_step} random token rows of the M={M_TOK} layer per step (rows are "
                                    f"independent, so the row-sampled oracle is exact for them); fp64 numpy"},
@@ -367,10 +374,8 @@ def main():
         "metric": METRIC, "value": round(value, 2), "unit": "TFLOPS", "n_gpus": W, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"llama7b_mlp_w{W}", "M": M_TOK, "H": HID, "I": FFN, "world": W, "act": "silu_mul",
-                   "gemm1": f"[{M_TOK}x{HID}] x [{2 * Il}x{HID}]^T", "gemm2": f"[{M_TOK}x{Il}] x [{HID}x{Il}]^T",
-                   "parallelism": f"tp{W}", "l2": "inputs larger than L2 (W1 180 MB + W2 90 MB + X 64 MB > 126 MB)",
-                   "cta_pair": comm.get_option("cta_pair")},
+        "config": bench_config(W),
+        "options": {k: comm.get_option(k) for k in ("cta_pair", "n_sub", "raster_group", "comm_tile_rows", "rs_order")},
         "tflops_per_gpu": round(per_gpu, 2),
         "kernels_ms": {"ag_gemm_silu": round(k1_ms, 4), "gemm_rs": round(k2_ms, 4)},
         "roofline": {"bound": "tensor", "kernel": "tl_gemm_kernel (AG-GEMM1 + SiLU*up)", "achieved": round(ach1, 2),
