@@ -340,28 +340,36 @@ def main():
         w28 = [t.cuda() for t in W2s8]
         o8 = [torch.empty(M_TOK // LW, HID, device="cuda", dtype=torch.bfloat16) for _ in range(LW)]
         z8 = [torch.empty(M_TOK, FFN // LW, device="cuda", dtype=torch.bfloat16) for _ in range(LW)]
-        for _ in range(args.warmup):
-            lc.ag_gemm_lb(xs8, w18, z8, act=tl.ACT_SILU_MUL)
-            lc.gemm_rs_lb(z8, w28, o8)
-        torch.cuda.synchronize()
-        le = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-        for i in range(args.steps):
-            le[i][0].record(stream)
-            lc.ag_gemm_lb(xs8, w18, z8, act=tl.ACT_SILU_MUL)
-            le[i][1].record(stream)
-            lc.gemm_rs_lb(z8, w28, o8)
-            le[i][2].record(stream)
-        torch.cuda.synchronize()
-        lst, ldiag = lc.check()
-        l1 = sum(e[0].elapsed_time(e[1]) for e in le) / args.steps
-        l2 = sum(e[1].elapsed_time(e[2]) for e in le) / args.steps
+
+        def lb_time(binding):
+            lc.set_option("ag_binding", binding)
+            for _ in range(args.warmup):
+                lc.ag_gemm_lb(xs8, w18, z8, act=tl.ACT_SILU_MUL)
+                lc.gemm_rs_lb(z8, w28, o8)
+            torch.cuda.synchronize()
+            le = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+            for i in range(args.steps):
+                le[i][0].record(stream)
+                lc.ag_gemm_lb(xs8, w18, z8, act=tl.ACT_SILU_MUL)
+                le[i][1].record(stream)
+                lc.gemm_rs_lb(z8, w28, o8)
+                le[i][2].record(stream)
+            torch.cuda.synchronize()
+            lst, _ = lc.check()
+            l1 = sum(e[0].elapsed_time(e[1]) for e in le) / args.steps
+            l2 = sum(e[1].elapsed_time(e[2]) for e in le) / args.steps
+            return l1, l2, lst
         from oracle import tl_oracle as O
         rows = [0, 1000, 2047, 3000, 5000, 8191]
         f = lambda L: [TI.to_f64(t) for t in L]
         ref = O.mlp_forward_rows(f(Xs8), f(W1s8), f(W2s8), TI.ACT_SILU_MUL, rows)
         mr8 = M_TOK // LW
-        got = np.stack([o8[i // mr8][i % mr8].float().cpu().double().numpy() for i in rows])
-        loop = {"world": LW, "mode": "loopback (8 ranks on 1 GPU, 18 CTAs each; peer stores -> local HBM)",
+        loop = {"world": LW, "mode": "loopback (8 ranks on 1 GPU, 18 CTAs each; peer stores -> local HBM; "
+                                      "the 8 ranks share one L2, so this is a protocol check, not a perf config)"}
+        for binding, name in ((0, "sm"), (1, "copy_engine")):
+            l1, l2, lst = lb_time(binding)
+            got = np.stack([o8[i // mr8][i % mr8].float().cpu().double().numpy() for i in rows])
+            loop[f"ag_binding_{name}"] = {
                 "ag_gemm_ms": round(l1, 4), "gemm_rs_ms": round(l2, 4), "ms_per_step": round(l1 + l2, 4),
                 "value": round((f1 + f2) / (l1 + l2) / 1e9, 2), "unit": "TFLOPS (whole layer, 1 GPU)",
                 "status": int(lst), "parity_rel_fro": O.rel_frobenius(got, np.stack([ref[i] for i in rows]))}

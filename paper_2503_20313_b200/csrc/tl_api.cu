@@ -75,6 +75,20 @@ struct WsLayout {
 };
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+PFN_cuStreamWriteValue32_v11070 g_write_value = nullptr;
+
+// rank_notify for the copy-engine binding: a stream memory operation executed
+// by the GPU front end after the preceding copy, with a system-wide fence before the write.
+tl_status get_write_value() {
+  if (g_write_value) return TL_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || fn == nullptr || q != cudaDriverEntryPointSuccess)
+    return fail(TL_ERR_UNSUPPORTED, "cuStreamWriteValue32 unavailable: copy-engine binding not supported");
+  g_write_value = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fn);
+  return TL_OK;
+}
 
 tl_status get_encode() {
   if (g_encode) return TL_OK;
@@ -108,7 +122,7 @@ tl_status make_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t col
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 8, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0;
+          n_sub = 0, ag_binding = 0, dma_tile_rows = 0;
 };
 
 struct OptDesc {
@@ -128,6 +142,8 @@ const OptDesc kOpts[] = {
     {"debug_drop_notify", &Options::debug_drop_notify, -1, 1 << 30},
     {"debug_drop_rank", &Options::debug_drop_rank, -1, kMaxWorld - 1},
     {"n_sub", &Options::n_sub, 0, 2},
+    {"ag_binding", &Options::ag_binding, 0, 1},
+    {"dma_tile_rows", &Options::dma_tile_rows, 0, 1 << 20},
 };
 
 }  // namespace
@@ -144,6 +160,9 @@ struct tl_comm {
   void* z[kMaxWorld] = {};          // local Z workspaces (mlp_forward with Z_ws = NULL)
   size_t z_bytes[kMaxWorld] = {};
   std::map<std::tuple<const void*, uint64_t, uint64_t, uint32_t, uint32_t>, CUtensorMap> tmaps;
+  // copy-engine binding of the AllGather (option ag_binding = 1): one copy stream per local rank
+  cudaStream_t copy_stream[kMaxWorld] = {};
+  cudaEvent_t ev_start = nullptr, ev_done[kMaxWorld] = {};
 };
 
 namespace {
@@ -323,7 +342,11 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
       return fail(TL_ERR_INVALID, "pointers must be 16-byte aligned");
   }
   const int64_t M_r = M / W;
-  StaticMap sm = StaticMap::make((int)M, W, (int)std::max<int64_t>(1, std::min<int64_t>(c->opt.comm_tile_rows, M_r)),
+  const bool dma = W > 1 && c->opt.ag_binding == 1;
+  int64_t tm = c->opt.comm_tile_rows;
+  if (dma)  // copy-engine binding: few large copies (each costs a host call), default 4 per rank
+    tm = c->opt.dma_tile_rows > 0 ? c->opt.dma_tile_rows : std::max<int64_t>(64, (M_r / 4 + 7) / 8 * 8);
+  StaticMap sm = StaticMap::make((int)M, W, (int)std::max<int64_t>(1, std::min<int64_t>(tm, M_r)),
                                  (int)c->opt.channels_per_rank);
   if (W > 1 && sm.tiles_per_rank > kAgFlagStride)
     return fail(TL_ERR_UNSUPPORTED, "too many producer tiles per rank (%d > %d): raise comm_tile_rows",
@@ -389,9 +412,54 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
     }
     if ((st = cached_tmap(c, &ra.tm_c, C[i], M, N_out, 32, 64)) != TL_OK) break;
   }
+  if (st == TL_OK && dma) {
+    // rank_copy_data + rank_notify on the copy engines ("maps AllGather to the DMA
+    // engine"): tile-major, self first; the GEMM kernel's consumer waits are unchanged.
+    p.copy_ctas = 0;
+    st = get_write_value();
+    if (st == TL_OK && !c->copy_stream[0]) {
+      cudaError_t e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
+      for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
+        e = cudaStreamCreateWithFlags(&c->copy_stream[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming);
+      }
+      if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "copy stream setup: %s", cudaGetErrorString(e));
+    }
+    if (st == TL_OK) {
+      cudaError_t e = cudaEventRecord(c->ev_start, stream);
+      for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) e = cudaStreamWaitEvent(c->copy_stream[i], c->ev_start, 0);
+      for (int t = 0; e == cudaSuccess && t < sm.tiles_per_rank; ++t) {
+        const int64_t lo = (int64_t)t * sm.Tm, hi = std::min<int64_t>(lo + sm.Tm, M_r);
+        for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
+          const int r = local_rank_id(c, i);
+          for (int dd = 0; e == cudaSuccess && dd < W; ++dd) {
+            const int d = (r + dd) % W;
+            uint8_t* dst = c->ws[d] + c->lay.xfull[bank] + ((size_t)r * M_r + lo) * K * 2;
+            e = cudaMemcpyAsync(dst, (const uint8_t*)A[i] + (size_t)lo * K * 2, (size_t)(hi - lo) * K * 2,
+                                cudaMemcpyDeviceToDevice, c->copy_stream[i]);
+            if (e != cudaSuccess) break;
+            uint32_t* flag = reinterpret_cast<uint32_t*>(c->ws[d] + c->lay.ag_flags) + r * kAgFlagStride + t;
+            const bool drop = r == c->opt.debug_drop_rank && t == c->opt.debug_drop_notify && d == (r + 1) % W;
+            if (!drop && g_write_value(c->copy_stream[i], (CUdeviceptr)flag, epoch, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+                             CUDA_SUCCESS)
+              e = cudaErrorUnknown;
+          }
+        }
+      }
+      if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "copy-engine AllGather enqueue failed: %s", cudaGetErrorString(e));
+    }
+  }
   if (st == TL_OK) {
     const int epi = act == TL_ACT_NONE ? EPI_STORE : act == TL_ACT_SILU_MUL ? EPI_SILU_MUL : EPI_GELU_MUL;
     st = launch(c, p, epi, comm, nsub, stream);
+  }
+  if (st == TL_OK && dma) {  // join: later work on `stream` is ordered after every copy
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
+      e = cudaEventRecord(c->ev_done[i], c->copy_stream[i]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, c->ev_done[i], 0);
+    }
+    if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "copy stream join: %s", cudaGetErrorString(e));
   }
   delete pp;
   if (st != TL_OK) return st;
@@ -665,6 +733,11 @@ tl_status tl_comm_destroy(tl_comm_t c) {
   }
   for (int i = 0; i < kMaxWorld; ++i)
     if (c->z[i]) cudaFree(c->z[i]);
+  for (int i = 0; i < kMaxWorld; ++i) {
+    if (c->copy_stream[i]) cudaStreamDestroy(c->copy_stream[i]);
+    if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+  }
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
   delete c;
   return TL_OK;
 }

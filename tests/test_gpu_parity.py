@@ -347,3 +347,58 @@ def test_split_tail_items(tl, act):
     torch.cuda.synchronize()
     _, Y = O.ag_gemm([TI.to_f64(A[0])], [TI.to_f64(Bs[0])])
     assert O.rel_frobenius(f64(C), O.activation(Y[0], act)) < TOL
+
+
+# ----------------------------------------------------------------------------- copy-engine AG binding (NEXT-1)
+@pytest.mark.parametrize("W", [2, 4, 8])
+@pytest.mark.parametrize("act", [TI.ACT_NONE, TI.ACT_SILU_MUL])
+def test_ag_dma_binding_parity(tl, W, act):
+    """AllGather on the copy engines (cudaMemcpyAsync + stream write-value flags, the paper's
+    benchmarked binding) feeding the same consumer waits: placement bit-exact + parity."""
+    M, K, N = 256 * W, 320, 200 if act else 392
+    As, Bs = TI.ag_gemm_inputs(M, (2 if act else 1) * N, K, W, seed=W + 40)
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=K)
+    c.set_option("ag_binding", 1)
+    Cs = [empty(M, N) for _ in range(W)]
+    Ag = [empty(M, K) for _ in range(W)]
+    c.ag_gemm_lb([cuda(a) for a in As], [cuda(b) for b in Bs], Cs, Ag, act=act)
+    st, diag = c.check()
+    assert st == 0, diag
+    full = torch.cat(As, 0)
+    _, Y = O.ag_gemm([TI.to_f64(a) for a in As], [TI.to_f64(b) for b in Bs])
+    for r in range(W):
+        assert torch.equal(Ag[r].cpu().view(torch.int16), full.view(torch.int16))
+        assert O.rel_frobenius(f64(Cs[r]), O.activation(Y[r], act)) < TOL
+
+
+def test_ag_dma_binding_matches_sm_binding_and_epochs(tl):
+    W, M, H, I = 4, 1024, 256, 1024
+    X, G, U, W2 = TI.mlp_full(M, H, I, seed=8)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    args = ([cuda(x) for x in Xs], [cuda(w) for w in W1s], [cuda(w) for w in W2s])
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=H)
+    ref = [empty(M // W, H) for _ in range(W)]
+    c.mlp_forward_lb(*args, ref, act=TI.ACT_SILU_MUL)
+    c.set_option("ag_binding", 1)
+    for i in range(12):   # banks and epochs cycle; DMA and SM bindings give identical bits
+        outs = [empty(M // W, H) for _ in range(W)]
+        c.set_option("dma_tile_rows", [0, 64, 128][i % 3])
+        c.mlp_forward_lb(*args, outs, act=TI.ACT_SILU_MUL)
+        for r in range(W):
+            assert torch.equal(outs[r], ref[r]), f"call {i} rank {r}"
+    assert c.check()[0] == 0
+
+
+def test_ag_dma_dropped_notify_times_out(tl):
+    W, M, K, N = 2, 512, 64, 128
+    As, Bs = TI.ag_gemm_inputs(M, N, K, W, seed=2)
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=K)
+    c.set_option("ag_binding", 1)
+    c.set_option("timeout_ms", 200)
+    c.set_option("debug_drop_rank", 1)
+    c.set_option("debug_drop_notify", 0)
+    Cs = [empty(M, N) for _ in range(W)]
+    c.ag_gemm_lb([cuda(a) for a in As], [cuda(b) for b in Bs], Cs)
+    st, diag = c.check()
+    assert st == 4
+    assert diag[1:5] == [0, 1, 1, 0]   # waiting rank 0, AG wait, source rank 1, producer tile 0
