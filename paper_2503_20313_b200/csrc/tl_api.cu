@@ -121,7 +121,7 @@ tl_status make_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t col
 
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
-          raster_group = 8, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
+          raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
           n_sub = 0, ag_binding = 0, dma_tile_rows = 0;
 };
 

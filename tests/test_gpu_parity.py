@@ -402,3 +402,34 @@ def test_ag_dma_dropped_notify_times_out(tl):
     st, diag = c.check()
     assert st == 4
     assert diag[1:5] == [0, 1, 1, 0]   # waiting rank 0, AG wait, source rank 1, producer tile 0
+
+
+# ----------------------------------------------------------------------------- full-size sampled parity
+@pytest.mark.parametrize("name,M,H,I,W", [
+    ("llama7b", 8192, 4096, 11008, 1),      # bench.py's N=1 workload and launch configuration
+    ("llama7b", 8192, 4096, 11008, 8),      # BASELINE configs[1] (8 ranks, loopback on one GPU)
+    ("llama70b", 8192, 8192, 28672, 2),     # configs[2] at W=2
+    ("mixtral", 16384, 4096, 14336, 4),     # configs[3] at W=4
+])
+def test_full_size_sampled_rows(tl, name, M, H, I, W):
+    """Full BASELINE.json sizes; the oracle is evaluated exactly on sampled rows (rows are
+    independent), spread over every rank's output block."""
+    X, G, U, W2 = TI.mlp_full(M, H, I, seed=0)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    Mr = M // W
+    outs = [empty(Mr, H) for _ in range(W)]
+    if W == 1:
+        c = tl.Comm.single(0, max_M=M, max_H=H)
+        c.mlp_forward(cuda(Xs[0]), cuda(W1s[0]), cuda(W2s[0]), outs[0], act=TI.ACT_SILU_MUL)
+        torch.cuda.synchronize()
+    else:
+        c = tl.Comm.loopback(W, 0, max_M=M, max_H=H)
+        c.mlp_forward_lb([cuda(x) for x in Xs], [cuda(w) for w in W1s], [cuda(w) for w in W2s], outs,
+                         act=TI.ACT_SILU_MUL)
+        assert c.check()[0] == 0
+    rows = sorted({r * Mr + o for r in range(W) for o in (0, Mr // 2, Mr - 1)} | {M // 3, 2 * M // 3})
+    ref = O.mlp_forward_rows([TI.to_f64(t) for t in Xs], [TI.to_f64(t) for t in W1s], [TI.to_f64(t) for t in W2s],
+                             TI.ACT_SILU_MUL, rows)
+    got = np.stack([outs[i // Mr][i % Mr].float().cpu().double().numpy() for i in rows])
+    assert O.rel_frobenius(got, np.stack([ref[i] for i in rows])) < TOL
+    del c
