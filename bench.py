@@ -366,6 +366,27 @@ def main():
         mr8 = M_TOK // LW
         loop = {"world": LW, "mode": "loopback (8 ranks on 1 GPU, 18 CTAs each; peer stores -> local HBM; "
                                       "the 8 ranks share one L2, so this is a protocol check, not a perf config)"}
+        # overlap ratio of the fused AG-GEMM: (comp_only + comm_only - overlap) / comm_only, with
+        # comp_only = the same launch without AllGather traffic, comm_only = only the copy role
+        def ag_ms(mode, n=args.steps):
+            lc.set_option("debug_mode", mode)
+            lc.ag_gemm_lb(xs8, w18, z8, act=tl.ACT_SILU_MUL)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(n):
+                lc.ag_gemm_lb(xs8, w18, z8, act=tl.ACT_SILU_MUL)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            lc.set_option("debug_mode", 0)
+            return a0.elapsed_time(a1) / n
+        for binding, name in ((0, "sm"), (1, "copy_engine")):
+            lc.set_option("ag_binding", binding)
+            ov, cp, cm = ag_ms(0), ag_ms(1), ag_ms(2)
+            loop[f"overlap_ratio_ag_{name}"] = {"comp_only_ms": round(cp, 4), "comm_only_ms": round(cm, 4),
+                                                "overlap_ms": round(ov, 4),
+                                                "ratio": round((cp + cm - ov) / cm, 4) if cm > 0 else None}
+        lc.check()
         for binding, name in ((0, "sm"), (1, "copy_engine")):
             l1, l2, lst = lb_time(binding)
             got = np.stack([o8[i // mr8][i % mr8].float().cpu().double().numpy() for i in rows])

@@ -106,7 +106,15 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *   "debug_drop_notify" (fault injection) index g >= 0 of one AG producer-tile notify to skip
  *                      on rank "debug_drop_rank" (default -1 = off); the waiting rank reports
  *                      TL_ERR_TIMEOUT instead of hanging
- *   "debug_drop_rank"  see above */
+ *   "debug_drop_rank"  see above
+ *   "ag_binding"       AllGather resource binding: 0 = SMs (bulk-copy warp in every CTA),
+ *                      1 = copy engines (cudaMemcpyAsync + stream write-value flags)
+ *   "dma_tile_rows"    producer-tile rows for ag_binding = 1 (default 0 = M/world/4, >= 64)
+ *   "n_sub"            256-column MMA sub-tiles per tile: 0 = auto, 1 = 256-wide (TMEM double-buffered),
+ *                      2 = 512-wide (less L2 traffic, un-overlapped epilogue)
+ *   "debug_mode"       overlap-ratio measurement: 0 normal, 1 computation only (no AG
+ *                      copies or waits; results are garbage unless X_full already holds the data),
+ *                      2 communication only (only the AG copy role runs) */
 tl_status tl_set_option(tl_comm_t comm, const char* key, int64_t value);
 tl_status tl_get_option(tl_comm_t comm, const char* key, int64_t* value);
 

@@ -122,7 +122,7 @@ tl_status make_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t col
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, dma_tile_rows = 0;
+          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0;
 };
 
 struct OptDesc {
@@ -144,6 +144,7 @@ const OptDesc kOpts[] = {
     {"n_sub", &Options::n_sub, 0, 2},
     {"ag_binding", &Options::ag_binding, 0, 1},
     {"dma_tile_rows", &Options::dma_tile_rows, 0, 1 << 20},
+    {"debug_mode", &Options::debug_mode, 0, 2},
 };
 
 }  // namespace
@@ -318,6 +319,7 @@ void fill_common(tl_comm* c, Params& p) {
   p.diag = reinterpret_cast<Diag*>(c->ws[c->loopback ? 0 : c->rank] + c->lay.diag);
   p.drop_rank = (int)c->opt.debug_drop_rank;
   p.drop_index = (int)c->opt.debug_drop_notify;
+  p.debug_mode = (int)c->opt.debug_mode;
 }
 
 // ---------------------------------------------------------------- AG-GEMM (+ act)
@@ -412,7 +414,8 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
     }
     if ((st = cached_tmap(c, &ra.tm_c, C[i], M, N_out, 32, 64)) != TL_OK) break;
   }
-  if (st == TL_OK && dma) {
+  if (p.debug_mode == 1) p.copy_ctas = 0;   // computation only: no AllGather traffic at all
+  if (st == TL_OK && dma && p.debug_mode != 1) {
     // rank_copy_data + rank_notify on the copy engines ("maps AllGather to the DMA
     // engine"): tile-major, self first; the GEMM kernel's consumer waits are unchanged.
     p.copy_ctas = 0;
@@ -596,6 +599,8 @@ tl_status alloc_ws(tl_comm* c, int r) {
   c->ws[r] = reinterpret_cast<uint8_t*>(p);
   c->owned[r] = true;
   TL_CUDA(cudaMemset(c->ws[r] + c->lay.flags_begin(), 0, c->lay.flags_bytes()));
+  // the zeroed flags must be in place before the handle exchange lets any peer write into them
+  TL_CUDA(cudaDeviceSynchronize());
   return TL_OK;
 }
 

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
   const int pair = cta_in_rank / kPair, n_pairs = p.ctas_per_rank / kPair;
   const RankArgs& ra = p.rk[lr];
   const int rank = ra.rank;
-  const int total = p.n_items;
+  const int total = p.debug_mode == 2 ? 0 : p.n_items;
   constexpr int BM = 128 * kPair;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::off_bar);
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         tile_coords(p, rank, ra.m_rot, t, mb, nb);
         const int row0 = mb * BM + cta_in_pair * 128;
         if constexpr (kAG) {
-          if (row0 < p.M) ag_wait_rows(p, rank, row0, min(row0 + 128, p.M));
+          if (p.debug_mode != 1 && row0 < p.M) ag_wait_rows(p, rank, row0, min(row0 + 128, p.M));
         }
         // the sub-tile count is a compile-time constant inside the k-loop (hoisted branch)
         auto produce = [&](auto ns_c, int s_lo) {

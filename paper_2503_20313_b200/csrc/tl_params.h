@@ -48,6 +48,9 @@ struct alignas(64) Params {
   // RS
   int rs_mode;
   int drop_rank, drop_index;
+  // overlap-ratio measurement: 0 = normal, 1 = computation only (no AG copies or waits,
+  // A read from whatever X_full holds), 2 = communication only (only the AG copy role runs)
+  int debug_mode;
 };
 
 }  // namespace tl
