@@ -50,8 +50,8 @@ def lib(build_if_missing: bool = True):
     global _LIB
     if _LIB is not None:
         return _LIB
-    path = _build.LIB
-    if build_if_missing and not _build.up_to_date():
+    path = os.environ.get("TL_LIB_PATH", _build.LIB)   # experiments only: A/B of two builds
+    if path == _build.LIB and build_if_missing and not _build.up_to_date():
         try:
             _build.build()
         except Exception:

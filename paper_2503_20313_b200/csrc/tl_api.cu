@@ -498,7 +498,7 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
   if (W > 1) {
     if (M_r % 128) return fail(TL_ERR_UNSUPPORTED, "GEMM-RS with world > 1 needs (M/world) %% 128 == 0 (M/world=%lld)",
                                (long long)M_r);
-    if ((M_r / 128) * n_blocks * nsub > kRsFlagStride)
+    if ((M_r / 128) * n_blocks * nsub * 4 > kRsFlagStride)
       return fail(TL_ERR_UNSUPPORTED, "too many RS tiles per owner block");
   }
   for (int i = 0; i < c->n_local; ++i) {

@@ -402,15 +402,17 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         const int W = p.world;
         const int o = row0 / p.M_r;                 // owner of these rows (offset in the global view)
         const int lrow0 = row0 - o * p.M_r;         // first row inside the owner's block
-        tile = (lrow0 / 128) * (p.n_blocks * kNSub) + nb * kNSub + sub_lo;   // flag per 128 x 256 sub-tile
+        // flags per (128-row block, 256-column sub-tile, 32-row warp slice): every epilogue warp
+        // notifies / waits its own slice, so there is no cross-warp barrier on the push path
+        tile = ((lrow0 / 128) * (p.n_blocks * kNSub) + nb * kNSub + sub_lo) * 4 + ew;
         myrow = lrow0 + ew * 32 + (int)lane;
         stg = p.staging[rank];
         if (p.rs_mode == RS_RING) {
           const int step = (o - rank - 1 + 2 * W) % W;   // o = r+1 -> 0, ..., o = r -> W-1
           if (step > 0) {                                // peer_tile_wait on the partial from rank r+1
             if ((int)lane < sub_n)
-              tile_wait(p.rs_flags[rank] + o * kRsFlagStride + tile + lane, p.epoch, p.timeout_ns, p.diag, rank, 2,
-                        (rank + 1) % W, tile + lane);
+              tile_wait(p.rs_flags[rank] + o * kRsFlagStride + tile + 4 * lane, p.epoch, p.timeout_ns, p.diag, rank,
+                        2, (rank + 1) % W, tile + 4 * lane);
             __syncwarp();
             add_mask = 1u << o;
           }
@@ -424,8 +426,8 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
           if (!push) {                                   // owner: peer_tile_wait on every other slot
             for (int q = 0; q < sub_n; ++q)
               if ((int)lane < W && (int)lane != rank)
-                tile_wait(p.rs_flags[rank] + lane * kRsFlagStride + tile + q, p.epoch, p.timeout_ns, p.diag, rank,
-                          2, lane, tile + q);
+                tile_wait(p.rs_flags[rank] + lane * kRsFlagStride + tile + 4 * q, p.epoch, p.timeout_ns, p.diag,
+                          rank, 2, lane, tile + 4 * q);
             __syncwarp();
             add_mask = ((1u << W) - 1) & ~(1u << rank);
           }
@@ -476,13 +478,14 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         if (pc + 2 < pc_end) ptx::tmem_ld_wait_fence<kPW>(ra_);
       }
       if constexpr (kEpi == EPI_RS) {
-        if (push) {
-          // every byte of this half-tile has landed in the target's slot -> notify (release)
-          if (lane == 0) ptx::bulk_wait<0>();
-          __syncwarp();
-          ptx::named_bar_sync(1, 128);
-          if (ew == 0 && (int)lane < sub_n) tile_notify(p.rs_flags[tgt] + slot * kRsFlagStride + tile + lane, p.epoch);
+        // peer_tile_notify per warp slice: once every byte this warp pushed has landed in the
+        // target's slot (its own bulk groups complete), release its slice flag(s).  The TMEM
+        // buffer was already released, so the wait overlaps the next tile's MMAs.
+        if (push && lane == 0) {
+          ptx::bulk_wait<0>();
+          for (int q = 0; q < sub_n; ++q) tile_notify(p.rs_flags[tgt] + slot * kRsFlagStride + tile + 4 * q, p.epoch);
         }
+        __syncwarp();
       }
     }
     if (lane == 0) ptx::bulk_wait<0>();
