@@ -433,3 +433,65 @@ def test_full_size_sampled_rows(tl, name, M, H, I, W):
     got = np.stack([outs[i // Mr][i % Mr].float().cpu().double().numpy() for i in rows])
     assert O.rel_frobenius(got, np.stack([ref[i] for i in rows])) < TOL
     del c
+
+
+# ----------------------------------------------------------------------------- odd worlds / option matrix
+@pytest.mark.parametrize("W", [3, 5, 6, 7])
+@pytest.mark.parametrize("ring", [0, 1])
+def test_mlp_odd_worlds(tl, W, ring):
+    """Non-power-of-two world sizes (ring successor/predecessor arithmetic, rotations, 128-row owner
+    blocks that straddle 256-row pair tiles when M/W is an odd multiple of 128)."""
+    M, H, I = 128 * W * (1 if W % 2 else 2), 192, 96 * W
+    X, G, U, W2 = TI.mlp_full(M, H, I, seed=W)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=H)
+    c.set_option("rs_order", ring)
+    outs = [empty(M // W, H) for _ in range(W)]
+    c.mlp_forward_lb([cuda(x) for x in Xs], [cuda(w) for w in W1s], [cuda(w) for w in W2s], outs,
+                     act=TI.ACT_SILU_MUL)
+    st, diag = c.check()
+    assert st == 0, diag
+    ref = O.mlp_forward([TI.to_f64(x) for x in Xs], [TI.to_f64(w) for w in W1s], [TI.to_f64(w) for w in W2s],
+                        TI.ACT_SILU_MUL)
+    assert O.rel_frobenius(np.concatenate([f64(o) for o in outs], 0), np.concatenate(ref, 0)) < TOL
+
+
+@pytest.mark.parametrize("opts", [
+    {"cta_pair": 1},
+    {"n_sub": 2, "ag_binding": 1},
+    {"n_sub": 1, "rs_order": 1, "comm_tile_rows": 16},
+    {"n_sub": 2, "rs_order": 1, "channels_per_rank": 1, "copy_ctas": 2},
+    {"raster_group": 1, "num_ctas": 8},
+    {"raster_group": 3, "num_ctas": 30, "n_sub": 2},
+])
+def test_mlp_option_matrix(tl, opts):
+    W, M, H, I = 4, 1024, 320, 1536
+    X, G, U, W2 = TI.mlp_full(M, H, I, seed=11)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=H)
+    for k, v in opts.items():
+        c.set_option(k, v)
+    outs = [empty(M // W, H) for _ in range(W)]
+    for _ in range(3):
+        c.mlp_forward_lb([cuda(x) for x in Xs], [cuda(w) for w in W1s], [cuda(w) for w in W2s], outs,
+                         act=TI.ACT_SILU_MUL)
+    st, diag = c.check()
+    assert st == 0, diag
+    ref = O.mlp_forward([TI.to_f64(x) for x in Xs], [TI.to_f64(w) for w in W1s], [TI.to_f64(w) for w in W2s],
+                        TI.ACT_SILU_MUL)
+    assert O.rel_frobenius(np.concatenate([f64(o) for o in outs], 0), np.concatenate(ref, 0)) < TOL
+
+
+def test_small_m_many_ranks(tl):
+    """M/W = 128 at W = 8 (the M = 1024 point of the M sweep): one CTA tile per owner block."""
+    W, M, H, I = 8, 1024, 256, 2048
+    X, G, U, W2 = TI.mlp_full(M, H, I, seed=13)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=H)
+    outs = [empty(M // W, H) for _ in range(W)]
+    c.mlp_forward_lb([cuda(x) for x in Xs], [cuda(w) for w in W1s], [cuda(w) for w in W2s], outs,
+                     act=TI.ACT_SILU_MUL)
+    assert c.check()[0] == 0
+    ref = O.mlp_forward([TI.to_f64(x) for x in Xs], [TI.to_f64(w) for w in W1s], [TI.to_f64(w) for w in W2s],
+                        TI.ACT_SILU_MUL)
+    assert O.rel_frobenius(np.concatenate([f64(o) for o in outs], 0), np.concatenate(ref, 0)) < TOL
