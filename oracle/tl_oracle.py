@@ -202,3 +202,40 @@ def rel_frobenius(got, ref) -> float:
     ref = np.asarray(ref, dtype=np.float64)
     den = np.linalg.norm(ref)
     return float(np.linalg.norm(got - ref) / den) if den > 0 else float(np.linalg.norm(got - ref))
+
+
+# ----------------------------------------------------------------------------
+# MoE first half: AllGather + Gather + GroupGEMM
+# ----------------------------------------------------------------------------
+def moe_group_rows(topk_ids, E: int):
+    """Grouped order of the routed rows (the dynamic shape mapping of P:422-431 made concrete):
+    every (token t, slot k) with expert e = topk_ids[t, k], sorted stably by (expert, token) --
+    tokens are rank-sharded contiguously, so this is (expert, source rank, token).
+    Returns a list of (e, t, k)."""
+    ids = np.asarray(topk_ids)
+    M, topk = ids.shape
+    rows = []
+    for t in range(M):
+        for k in range(topk):
+            e = int(ids[t, k])
+            if not 0 <= e < E:
+                raise ValueError("expert id out of range")
+            rows.append((e, t, k))
+    rows.sort(key=lambda x: (x[0], x[1]))   # Python's sort is stable: equal (e, t) keep slot order
+    return rows
+
+
+def moe_ag_group_gemm(X_shards, topk_ids, W1_list, act: int):
+    """AG + Gather + GroupGEMM: X = AllGather_rows(X_r); for every routed row
+    (e, t, k) in grouped order, Y_r[row] = act(X[t] . W1_r[e]^T), W1_r[e] in nn.Linear layout
+    ([N1, H]; [gate; up] halves for the *_MUL acts).  Returns (rows, [Y_r])."""
+    X = all_gather_rows(X_shards)
+    E = np.asarray(W1_list[0]).shape[0]
+    rows = moe_group_rows(topk_ids, E)
+    Ys = []
+    for W1 in W1_list:
+        W1 = np.asarray(W1, dtype=np.float64)
+        Y = np.stack([activation(X[t][None, :] @ W1[e].T, act)[0] for (e, t, k) in rows]) if rows else \
+            np.zeros((0, W1.shape[1] // (1 if act == ACT_NONE else 2)))
+        Ys.append(Y)
+    return rows, Ys

@@ -231,3 +231,43 @@ def test_rel_frobenius():
     a = np.array([3.0, 4.0])
     assert O.rel_frobenius(a, a) == 0.0
     assert O.rel_frobenius(np.array([3.0, 5.0]), a) == pytest.approx(0.2)
+
+
+# --- MoE first half (NEXT-3): pins ------------------------------------------------
+def test_moe_grouping_is_a_stable_permutation():
+    ids = np.array([[1, 0], [0, 2], [1, 2], [2, 1]])
+    rows = O.moe_group_rows(ids, 3)
+    assert rows == [(0, 0, 1), (0, 1, 0), (1, 0, 0), (1, 2, 0), (1, 3, 1), (2, 1, 1), (2, 2, 1), (2, 3, 0)]
+    ids = TI.moe_routing(64, 8, 3, seed=1).numpy()
+    rows = O.moe_group_rows(ids, 8)
+    assert sorted((t, k) for _, t, k in rows) == [(t, k) for t in range(64) for k in range(3)]   # S:374 conservation
+    assert all(ids[t, k] == e for e, t, k in rows)
+    assert rows == sorted(rows, key=lambda x: (x[0], x[1], x[2]))
+
+
+def test_moe_single_expert_is_plain_ag_gemm():
+    W, M, H, N1 = 2, 16, 8, 6
+    Xs, _ = TI.ag_gemm_inputs(M, N1, H, W, seed=2)
+    Ws = TI.moe_weights(1, N1, H, W, seed=3)
+    ids = np.zeros((M, 1), dtype=np.int64)
+    rows, Ys = O.moe_ag_group_gemm([TI.to_f64(x) for x in Xs], ids, [TI.to_f64(w) for w in Ws], O.ACT_NONE)
+    _, Cs = O.ag_gemm([TI.to_f64(x) for x in Xs], [TI.to_f64(w[0]) for w in Ws])
+    for r in range(W):
+        np.testing.assert_array_equal(Ys[r], Cs[r])   # identity routing: row j is token j
+
+
+def test_moe_pyloop_and_placement_closed_form():
+    W, M, H, E, N1 = 2, 12, 16, 3, 4
+    Xs, Ws = TI.moe_placement_inputs(M, H, E, N1, W)
+    ids = TI.moe_routing(M, E, 2, seed=4).numpy()
+    rows, Ys = O.moe_ag_group_gemm([TI.to_f64(x) for x in Xs], ids, [TI.to_f64(w) for w in Ws], O.ACT_NONE)
+    for r in range(W):
+        for j, (e, t, k) in enumerate(rows):
+            for n in range(N1):
+                assert Ys[r][j, n] == (t >> (4 * ((n + e + r) % 4))) & 15
+    # brute force, pure Python, one routed row at a time
+    X = [x for s in Xs for x in s.float().tolist()]
+    W1 = Ws[1].float().tolist()
+    for j, (e, t, k) in enumerate(rows):
+        for n in range(N1):
+            assert sum(a * b for a, b in zip(X[t], W1[e][n])) == Ys[1][j, n]

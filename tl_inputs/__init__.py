@@ -141,3 +141,38 @@ def rs_placement_inputs(M: int, N: int, K_local: int, W: int):
 def to_f64(t: torch.Tensor):
     """bf16 torch tensor -> float64 numpy array (exact: every bf16 value is an fp64 value)."""
     return t.to(torch.float64).numpy()
+
+
+def moe_routing(M: int, E: int, topk: int, seed: int = 0, skew: float = 0.0):
+    """Seeded top-k routing: topk distinct experts per token, int32 [M, topk].
+
+    skew = 0 draws experts uniformly; skew > 0 draws them with weights ~ (e + 1)^-skew (a few hot
+    experts, as real routers produce).  No arithmetic of the method."""
+    g = torch.Generator().manual_seed(int(seed) * 1000 + 7)
+    w = (torch.arange(E, dtype=torch.float64) + 1.0) ** (-float(skew))
+    ids = torch.multinomial(w.expand(M, E).contiguous(), topk, replacement=False, generator=g)
+    return ids.to(torch.int32)
+
+
+def moe_weights(E: int, N1: int, H: int, W: int, seed: int = 0):
+    """Per-rank expert weights [E, N1, H] bf16 ~ N(0, 1/H) (each rank's TP shard of every expert)."""
+    return [_randn((E, N1, H), seed + 13 * r, _TID_B, H ** -0.5) for r in range(W)]
+
+
+def moe_placement_inputs(M: int, H: int, E: int, N1: int, W: int):
+    """Index fixture for the gather: X[t, b] = bit_b(t) (b < 16), expert e's weight row n picks the
+    nibble (n + e) mod 4 -> Y[row, n] = nibble_{(n + e) mod 4}(t): exact, unique per (token, expert)."""
+    assert H >= 16
+    idx = torch.arange(M, dtype=torch.int64)
+    X = torch.zeros(M, H, dtype=torch.float32)
+    X[:, :16] = _bits(idx, 16).to(torch.float32)
+    Ws = []
+    for r in range(W):
+        B = torch.zeros(E, N1, H, dtype=torch.float32)
+        for e in range(E):
+            for n in range(N1):
+                q = (n + e + r) % 4
+                for j in range(4):
+                    B[e, n, 4 * q + j] = float(1 << j)
+        Ws.append(B.to(torch.bfloat16))
+    return shard_rows(X.to(torch.bfloat16), W), Ws
