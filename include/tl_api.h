@@ -170,6 +170,30 @@ tl_status tl_mlp_forward_loopback(tl_comm_t comm, const void* const* X_shard,
                                   void* const* out_shard, void* const* Z_ws, int64_t M,
                                   int64_t H, int64_t I_local, tl_act act, void* stream);
 
+/* ---------------------------------------------------------------- MoE first half (NEXT-3) --
+ * AllGather + Gather + GroupGEMM with the paper's *dynamic* tile-centric mapping
+ * (lookup tables filled at runtime from the routing):
+ *   Y[g, :] = act( AllGather_rows(X_shard)[token(g)] . W1[expert(g)]^T )
+ * for every routed row g of the grouped layout: all (token t, slot k) pairs sorted stably by
+ * (expert, token), each expert's group padded to a multiple of the tile height 128 * cta_pair.
+ *   X_shard   bf16 [M/world, H]            topk_ids int32 [M, topk] (global routing, identical on
+ *   W1        bf16 [E, N1, H], N1 = N_out (NONE) or 2 * N_out ([gate; up] per expert)   every rank)
+ *   Y         bf16 [R_cap, N_out]  (padding rows hold garbage)
+ *   row_ids   int32 [R_cap] out: t * topk + k of each grouped row, -1 for padding (16-byte aligned)
+ *   expert_offsets int32 [E + 1] out: padded group starts (group e = rows [off[e], off[e+1]))
+ *   R_cap = tl_moe_capacity(comm, M, topk, E) = roundup(M * topk + E * (BM - 1), BM).
+ * The tables are built on the device (no host synchronisation); a GEMM tile waits only on the
+ * producer tiles its (sorted) tokens live in, and tiles are scheduled in expected-arrival order.
+ * Constraints as tl_ag_gemm_act, plus 1 <= topk <= E <= 1024. */
+int64_t tl_moe_capacity(tl_comm_t comm, int64_t M, int topk, int E);
+tl_status tl_moe_ag_gemm(tl_comm_t comm, const void* X_shard, const int32_t* topk_ids, const void* W1, void* Y,
+                         int32_t* row_ids, int32_t* expert_offsets, int64_t M, int64_t H, int64_t N_out,
+                         int E, int topk, tl_act act, void* stream);
+tl_status tl_moe_ag_gemm_loopback(tl_comm_t comm, const void* const* X_shard,
+                                  const int32_t* const* topk_ids, const void* const* W1, void* const* Y,
+                                  int32_t* const* row_ids, int32_t* const* expert_offsets, int64_t M,
+                                  int64_t H, int64_t N_out, int E, int topk, tl_act act, void* stream);
+
 /* ---------------------------------------------------------------- diagnostics -------------
  * Evaluates the device-side static mapping for producer tiles t = 0..n-1 of a
  * gathered M-row tensor on `world` ranks with Tm_p rows per tile and C channels per rank, in a

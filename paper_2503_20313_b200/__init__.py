@@ -14,7 +14,8 @@ from ._lib import TLError, check, lib, ptr_array
 ACT_NONE, ACT_SILU_MUL, ACT_GELU_TANH_MUL = 0, 1, 2
 ACTS = {"none": ACT_NONE, "silu_mul": ACT_SILU_MUL, "gelu_tanh_mul": ACT_GELU_TANH_MUL}
 
-__all__ = ["Comm", "TLError", "lib", "ACT_NONE", "ACT_SILU_MUL", "ACT_GELU_TANH_MUL", "static_map_device"]
+__all__ = ["Comm", "TLError", "lib", "ACT_NONE", "ACT_SILU_MUL", "ACT_GELU_TANH_MUL", "static_map_device",
+           "moe_capacity", "moe_ag_gemm", "moe_ag_gemm_lb"]
 
 
 def _ptr(t):
@@ -163,6 +164,34 @@ class Comm:
         check(lib().tl_mlp_forward_loopback(self._h, x, w1, w2, o, z, M, H, I_l, act, _stream(stream)),
               "tl_mlp_forward_loopback")
         return outs
+
+
+def moe_capacity(comm, M: int, topk: int, E: int) -> int:
+    return lib().tl_moe_capacity(comm._h, M, topk, E)
+
+
+def moe_ag_gemm(comm, X_shard, topk_ids, W1, Y, row_ids, offsets, act: int = ACT_SILU_MUL, stream=None):
+    """MoE AG + Gather + GroupGEMM on a one-rank-per-process comm (see tl_api.h)."""
+    M = X_shard.shape[0] * comm.world
+    H = X_shard.shape[1]
+    E, topk = W1.shape[0], topk_ids.shape[1]
+    N_out = Y.shape[1]
+    check(lib().tl_moe_ag_gemm(comm._h, _ptr(X_shard), _ptr(topk_ids), _ptr(W1), _ptr(Y), _ptr(row_ids),
+                               _ptr(offsets), M, H, N_out, E, topk, act, _stream(stream)), "tl_moe_ag_gemm")
+    return Y
+
+
+def moe_ag_gemm_lb(comm, X_shards, topk_ids, W1s, Ys, row_ids, offsets, act: int = ACT_SILU_MUL, stream=None):
+    """Loopback variant: per-rank lists (topk_ids / row_ids / offsets are per-rank device copies)."""
+    W = comm.world
+    M = X_shards[0].shape[0] * W
+    H = X_shards[0].shape[1]
+    E, topk = W1s[0].shape[0], topk_ids[0].shape[1]
+    N_out = Ys[0].shape[1]
+    arrs = [ptr_array([_ptr(t) for t in L]) for L in (X_shards, topk_ids, W1s, Ys, row_ids, offsets)]
+    check(lib().tl_moe_ag_gemm_loopback(comm._h, *[a[0] for a in arrs], M, H, N_out, E, topk, act,
+                                        _stream(stream)), "tl_moe_ag_gemm_loopback")
+    return Ys
 
 
 def static_map_device(M: int, world: int, tm_rows: int, channels_per_rank: int, n: int):

@@ -35,6 +35,10 @@ SIGNATURES = {
     "tl_gemm_rs_loopback": (_int, [_vp, _vpp, _vpp, _vpp, _i64, _i64, _i64, _vp]),
     "tl_mlp_forward_loopback": (_int, [_vp, _vpp, _vpp, _vpp, _vpp, _vpp, _i64, _i64, _i64, _int, _vp]),
     "tl_debug_static_map": (_int, [_i64, _int, _i64, _int, _i64, C.POINTER(_i64)]),
+    "tl_moe_capacity": (_i64, [_vp, _i64, _int, _int]),
+    "tl_moe_ag_gemm": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _int, _vp]),
+    "tl_moe_ag_gemm_loopback": (_int, [_vp, _vpp, _vpp, _vpp, _vpp, _vpp, _vpp, _i64, _i64, _i64, _int, _int, _int,
+                                       _vp]),
 }
 
 

@@ -119,6 +119,22 @@ tl_status make_tmap(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t col
   return TL_OK;
 }
 
+// N-D bf16 tensor map: dims/box innermost first, strides in bytes for dims 1..rank-1.
+tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
+                       const uint32_t* box) {
+  tl_status s = get_encode();
+  if (s != TL_OK) return s;
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) d[i] = dims[i], b[i] = box[i], e[i] = 1;
+  for (int i = 0; i + 1 < rank; ++i) st[i] = strides[i];
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), d, st, b, e,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TL_ERR_CUDA, "cuTensorMapEncodeTiled(%d-D) failed: %d", rank, (int)r);
+  return TL_OK;
+}
+
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
@@ -164,6 +180,9 @@ struct tl_comm {
   // copy-engine binding of the AllGather (option ag_binding = 1): one copy stream per local rank
   cudaStream_t copy_stream[kMaxWorld] = {};
   cudaEvent_t ev_start = nullptr, ev_done[kMaxWorld] = {};
+  // MoE tile tables per local rank (device): tab [4 + 3 * max_tiles] ints, sched [max_tiles], err
+  int* moe_buf[kMaxWorld] = {};
+  size_t moe_bytes[kMaxWorld] = {};
 };
 
 namespace {
@@ -213,11 +232,11 @@ int ctas_per_rank(const tl_comm* c) {
   return n < pair ? pair : n;
 }
 
-template <int kPair, int kEpi, bool kAG, int kNSub>
+template <int kPair, int kEpi, bool kAG, int kNSub, bool kMoE = false>
 tl_status launch_t(tl_comm* c, const Params& p, cudaStream_t stream) {
   constexpr int kStages = stages_for(kPair, kAG, kNSub);
   using L = Layout<kPair, kStages, kAG, kNSub>;
-  auto kern = tl_gemm_kernel<kPair, kStages, kEpi, kAG, kNSub>;
+  auto kern = tl_gemm_kernel<kPair, kStages, kEpi, kAG, kNSub, kMoE>;
   static bool attr_set = false;
   if (!attr_set) {
     TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::smem_request));
@@ -237,6 +256,22 @@ tl_status launch_t(tl_comm* c, const Params& p, cudaStream_t stream) {
   cfg.numAttrs = 1;
   TL_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
   return TL_OK;
+}
+
+tl_status launch_moe(tl_comm* c, const Params& p, int epi, bool ag, cudaStream_t s) {
+  const int pair = pair_of(c);
+  if (pair == 2) {
+    if (epi == EPI_STORE)
+      return ag ? launch_t<2, EPI_STORE, true, 1, true>(c, p, s) : launch_t<2, EPI_STORE, false, 1, true>(c, p, s);
+    if (epi == EPI_SILU_MUL)
+      return ag ? launch_t<2, EPI_SILU_MUL, true, 1, true>(c, p, s) : launch_t<2, EPI_SILU_MUL, false, 1, true>(c, p, s);
+    return ag ? launch_t<2, EPI_GELU_MUL, true, 1, true>(c, p, s) : launch_t<2, EPI_GELU_MUL, false, 1, true>(c, p, s);
+  }
+  if (epi == EPI_STORE)
+    return ag ? launch_t<1, EPI_STORE, true, 1, true>(c, p, s) : launch_t<1, EPI_STORE, false, 1, true>(c, p, s);
+  if (epi == EPI_SILU_MUL)
+    return ag ? launch_t<1, EPI_SILU_MUL, true, 1, true>(c, p, s) : launch_t<1, EPI_SILU_MUL, false, 1, true>(c, p, s);
+  return ag ? launch_t<1, EPI_GELU_MUL, true, 1, true>(c, p, s) : launch_t<1, EPI_GELU_MUL, false, 1, true>(c, p, s);
 }
 
 tl_status launch(tl_comm* c, const Params& p, int epi, bool ag, int nsub, cudaStream_t s) {
@@ -322,9 +357,23 @@ void fill_common(tl_comm* c, Params& p) {
   p.debug_mode = (int)c->opt.debug_mode;
 }
 
+// MoE first half (dynamic mapping): routing in, grouped tables out (per local rank).
+struct MoeArgs {
+  const int32_t* const* topk_ids;  // [M, topk]
+  int32_t* const* rows;            // [R_cap] out
+  int32_t* const* offs;            // [E + 1] out
+  int E, topk;
+  int64_t R_cap;
+};
+
+int64_t moe_capacity(int64_t M, int topk, int E, int BM) {
+  return (M * topk + (int64_t)E * (BM - 1) + BM - 1) / BM * BM;
+}
+
 // ---------------------------------------------------------------- AG-GEMM (+ act)
 tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, void* const* C,
-                       void* const* Agath, int64_t M, int64_t N_out, int64_t K, int act, cudaStream_t stream) {
+                       void* const* Agath, int64_t M, int64_t N_out, int64_t K, int act, cudaStream_t stream,
+                       const MoeArgs* moe = nullptr) {
   tl_status st = check_comm(c);
   if (st != TL_OK) return st;
   const int W = c->world;
@@ -337,8 +386,17 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
     return fail(TL_ERR_INVALID, "M=%lld K=%lld exceed comm capacity (%lld, %lld)", (long long)M, (long long)K,
                 (long long)c->max_M, (long long)c->max_H);
   if (M >= (1ll << 31) || N_out >= (1ll << 31) || K >= (1ll << 31)) return fail(TL_ERR_UNSUPPORTED, "dimension >= 2^31");
+  const int64_t c_rows = moe ? moe->R_cap : M;   // rows of the output (MoE: padded grouped rows)
+  if (moe) {
+    if (moe->E < 1 || moe->E > 1024 || moe->topk < 1 || moe->topk > moe->E)
+      return fail(TL_ERR_INVALID, "MoE needs 1 <= topk <= E <= 1024 (E=%d topk=%d)", moe->E, moe->topk);
+    if (M * moe->topk >= (1ll << 30)) return fail(TL_ERR_UNSUPPORTED, "too many routed rows");
+    for (int i = 0; i < c->n_local; ++i)
+      if (!moe->topk_ids[i] || !moe->rows[i] || !moe->offs[i] || !aligned16(moe->rows[i]))
+        return fail(TL_ERR_INVALID, "MoE table pointers must be non-null (row_ids 16-byte aligned)");
+  }
   for (int i = 0; i < c->n_local; ++i) {   // a pointer may be null only when its tensor is empty
-    if ((!A[i] && M * K) || (!B[i] && N_out * K) || (!C[i] && M * N_out))
+    if ((!A[i] && M * K) || (!B[i] && N_out * K) || (!C[i] && c_rows * N_out))
       return fail(TL_ERR_INVALID, "null pointer (rank slot %d)", i);
     if (!aligned16(A[i]) || !aligned16(B[i]) || !aligned16(C[i]) || (Agath && Agath[i] && !aligned16(Agath[i])))
       return fail(TL_ERR_INVALID, "pointers must be 16-byte aligned");
@@ -353,6 +411,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   if (W > 1 && sm.tiles_per_rank > kAgFlagStride)
     return fail(TL_ERR_UNSUPPORTED, "too many producer tiles per rank (%d > %d): raise comm_tile_rows",
                 sm.tiles_per_rank, kAgFlagStride);
+  if (moe && K == 0) return fail(TL_ERR_UNSUPPORTED, "MoE with K == 0");
   if (M == 0 || N_out == 0) return TL_OK;
   if (K == 0) {
     for (int i = 0; i < c->n_local; ++i) {
@@ -376,7 +435,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   p.M_r = (int)M_r;
   p.epoch = epoch;
   p.m_blocks = (int)((M + 128 * pair - 1) / (128 * pair));
-  const int nsub = choose_nsub(c, M, N_out, K, act != TL_ACT_NONE);
+  const int nsub = moe ? 1 : choose_nsub(c, M, N_out, K, act != TL_ACT_NONE);
   const int bn_out = (act ? 128 : 256) * nsub;
   p.n_blocks = (int)((N_out + bn_out - 1) / bn_out);
   p.k_blocks = (int)((K + kBK - 1) / kBK);
@@ -403,7 +462,25 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
     ra.a_shard = reinterpret_cast<const uint8_t*>(A[i]);
     ra.m_rot = (int)((r * M_r) / (128 * pair));
     const void* a_src = comm ? (const void*)(c->ws[r] + c->lay.xfull[bank]) : A[i];
-    if ((st = cached_tmap(c, &ra.tm_a, a_src, M, K, 128, 64)) != TL_OK) break;
+    if (moe) {
+      // A: row-gather map (box 64 x 1; tile::gather4 fetches 4 token rows per instruction)
+      if ((st = cached_tmap(c, &ra.tm_a, a_src, M, K, 1, 64)) != TL_OK) break;
+      // B: [E][N1][K] (plain) or [E][2][N_out][K] (gated: gate / up halves, out-of-range rows per half)
+      const uint64_t kb = (uint64_t)K * 2;
+      if (act == TL_ACT_NONE) {
+        const uint64_t dims[3] = {(uint64_t)K, (uint64_t)N_out, (uint64_t)moe->E};
+        const uint64_t str[2] = {kb, kb * N_out};
+        const uint32_t box[3] = {64, (uint32_t)(pair == 2 ? 128 : 256), 1};
+        if ((st = make_tmap_nd(&ra.tm_b0, B[i], 3, dims, str, box)) != TL_OK) break;
+      } else {
+        const uint64_t dims[4] = {(uint64_t)K, (uint64_t)N_out, 2, (uint64_t)moe->E};
+        const uint64_t str[3] = {kb, kb * N_out, kb * N_out * 2};
+        const uint32_t box[4] = {64, 128, 1, 1};
+        if ((st = make_tmap_nd(&ra.tm_b0, B[i], 4, dims, str, box)) != TL_OK) break;
+      }
+      if ((st = cached_tmap(c, &ra.tm_c, C[i], c_rows, N_out, 32, 64)) != TL_OK) break;
+      continue;
+    }
     if (act == TL_ACT_NONE) {
       if ((st = cached_tmap(c, &ra.tm_b0, B[i], N_out, K, pair == 2 ? 128 : 256, 64)) != TL_OK) break;
     } else {
@@ -452,9 +529,40 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
       if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "copy-engine AllGather enqueue failed: %s", cudaGetErrorString(e));
     }
   }
+  if (st == TL_OK && moe) {
+    // dynamic mapping tables, built on the device from the routing, per local rank
+    const int BM = 128 * pair;
+    const int max_tiles = (int)(moe->R_cap / BM);
+    p.topk = moe->topk;
+    const size_t need = (size_t)(4 + 3 * max_tiles + max_tiles + 4) * sizeof(int);
+    const size_t smem = (size_t)(2 * moe->E + 64 * moe->E + moe->E + 1 + max_tiles + kMoeThreads) * sizeof(int);
+    if (smem > 227 * 1024) st = fail(TL_ERR_UNSUPPORTED, "MoE table build needs %zu B of smem", smem);
+    for (int i = 0; st == TL_OK && i < c->n_local; ++i) {
+      if (c->moe_bytes[i] < need) {
+        if (c->moe_buf[i]) cudaFree(c->moe_buf[i]);
+        c->moe_buf[i] = nullptr;
+        c->moe_bytes[i] = 0;
+        cudaError_t e = cudaMalloc(&c->moe_buf[i], need);
+        if (e != cudaSuccess) { st = fail(TL_ERR_CUDA, "MoE table alloc: %s", cudaGetErrorString(e)); break; }
+        c->moe_bytes[i] = need;
+      }
+      int* tab = c->moe_buf[i];
+      int* sched = tab + 4 + 3 * max_tiles;
+      int* err = sched + max_tiles;
+      cudaFuncSetAttribute(tl_moe_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      tl_moe_tables_kernel<<<1, kMoeThreads, smem, stream>>>(moe->topk_ids[i], (int)(M * moe->topk), moe->topk,
+                                                             moe->E, BM, (int)M_r, sm.Tm, moe->rows[i], moe->offs[i],
+                                                             tab, sched, max_tiles, err);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) { st = fail(TL_ERR_CUDA, "MoE table kernel: %s", cudaGetErrorString(e)); break; }
+      p.rk[i].moe_rows = moe->rows[i];
+      p.rk[i].moe_tab = tab;
+      p.rk[i].moe_sched = sched;
+    }
+  }
   if (st == TL_OK) {
     const int epi = act == TL_ACT_NONE ? EPI_STORE : act == TL_ACT_SILU_MUL ? EPI_SILU_MUL : EPI_GELU_MUL;
-    st = launch(c, p, epi, comm, nsub, stream);
+    st = moe ? launch_moe(c, p, epi, comm, stream) : launch(c, p, epi, comm, nsub, stream);
   }
   if (st == TL_OK && dma) {  // join: later work on `stream` is ordered after every copy
     cudaError_t e = cudaSuccess;
@@ -743,6 +851,8 @@ tl_status tl_comm_destroy(tl_comm_t c) {
     if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
   }
   if (c->ev_start) cudaEventDestroy(c->ev_start);
+  for (int i = 0; i < kMaxWorld; ++i)
+    if (c->moe_buf[i]) cudaFree(c->moe_buf[i]);
   delete c;
   return TL_OK;
 }
@@ -843,6 +953,31 @@ tl_status tl_mlp_forward_loopback(tl_comm_t c, const void* const* X, const void*
   if (!c || !c->loopback) return fail(TL_ERR_STATE, "not a loopback comm");
   if (!X || !W1 || !W2 || !out) return fail(TL_ERR_INVALID, "null pointer array");
   return mlp_impl(c, X, W1, W2, out, Z, M, H, I_l, act, (cudaStream_t)stream);
+}
+
+int64_t tl_moe_capacity(tl_comm_t c, int64_t M, int topk, int E) {
+  const int BM = c ? 128 * pair_of(c) : 256;
+  return moe_capacity(M, topk, E, BM);
+}
+
+tl_status tl_moe_ag_gemm(tl_comm_t c, const void* X, const int32_t* topk_ids, const void* W1, void* Y,
+                         int32_t* row_ids, int32_t* expert_offsets, int64_t M, int64_t H, int64_t N_out, int E,
+                         int topk, tl_act act, void* stream) {
+  if (c && c->loopback) return fail(TL_ERR_STATE, "loopback comm: use tl_moe_ag_gemm_loopback");
+  if (!c) return fail(TL_ERR_INVALID, "null comm");
+  MoeArgs m{&topk_ids, &row_ids, &expert_offsets, E, topk, moe_capacity(M, topk, E, 128 * pair_of(c))};
+  void* ag[1] = {nullptr};
+  return ag_gemm_impl(c, &X, &W1, &Y, ag, M, N_out, H, act, (cudaStream_t)stream, &m);
+}
+
+tl_status tl_moe_ag_gemm_loopback(tl_comm_t c, const void* const* X, const int32_t* const* topk_ids,
+                                  const void* const* W1, void* const* Y, int32_t* const* row_ids,
+                                  int32_t* const* expert_offsets, int64_t M, int64_t H, int64_t N_out, int E, int topk,
+                                  tl_act act, void* stream) {
+  if (!c || !c->loopback) return fail(TL_ERR_STATE, "not a loopback comm");
+  if (!X || !topk_ids || !W1 || !Y || !row_ids || !expert_offsets) return fail(TL_ERR_INVALID, "null pointer array");
+  MoeArgs m{topk_ids, row_ids, expert_offsets, E, topk, moe_capacity(M, topk, E, 128 * pair_of(c))};
+  return ag_gemm_impl(c, X, W1, Y, nullptr, M, N_out, H, act, (cudaStream_t)stream, &m);
 }
 
 tl_status tl_debug_static_map(int64_t M, int world, int64_t tm_rows, int channels_per_rank, int64_t n, int64_t* out) {

@@ -48,7 +48,8 @@ struct Layout {
   // full[S], empty[S], tfull[2], tempty[2], copy[2]
   static constexpr int n_bars = 2 * kStages + 6;
   static constexpr int off_tmem = off_bar + n_bars * 8;
-  static constexpr int bytes = off_tmem + 16;
+  static constexpr int off_ids = off_tmem + 16;     // MoE: token ids of this CTA's 128 rows
+  static constexpr int bytes = off_ids + 512;
   static constexpr int smem_request = bytes + 1024;  // slack for manual 1024-byte alignment
 };
 
@@ -96,6 +97,17 @@ __device__ __forceinline__ void item_coords(const Params& p, int item, int& t, i
     sub_lo = j % kNSub;
     sub_n = 1;
   }
+}
+
+// MoE work item -> (m-tile of the padded grouped rows, n-block, expert).  Tiles run in the order
+// of the device-built schedule (by the producer tile their last token needs, i.e. by expected
+// arrival), n-blocks innermost so a gathered A block is reused from L2.
+__device__ __forceinline__ void moe_coords(const Params& p, const RankArgs& ra, int item, int& mt, int& nb,
+                                           int& expert) {
+  const int j = item / p.n_blocks;
+  nb = item - j * p.n_blocks;
+  mt = ra.moe_sched[j];
+  expert = ra.moe_tab[4 + 3 * mt];
 }
 
 // consumer_tile_wait for A rows [lo, hi) of the gathered tensor: every producer tile of every
@@ -179,7 +191,7 @@ __device__ __forceinline__ void epi_load(uint32_t tacc, int pc, float* r) {
   }
 }
 
-template <int kPair, int kStages, int kEpi, bool kAG, int kNSub>
+template <int kPair, int kStages, int kEpi, bool kAG, int kNSub, bool kMoE = false>
 __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_constant__ Params p) {
   using L = Layout<kPair, kStages, kAG, kNSub>;
   constexpr int kAccBufs = 2 / kNSub;          // TMEM accumulator buffers (512 columns in total)
@@ -194,7 +206,8 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
   const int pair = cta_in_rank / kPair, n_pairs = p.ctas_per_rank / kPair;
   const RankArgs& ra = p.rk[lr];
   const int rank = ra.rank;
-  const int total = p.debug_mode == 2 ? 0 : p.n_items;
+  // MoE: the number of m-tiles is data dependent (built on the device from the routing)
+  const int total = p.debug_mode == 2 ? 0 : kMoE ? ra.moe_tab[0] * p.n_blocks : p.n_items;
   constexpr int BM = 128 * kPair;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::off_bar);
@@ -234,12 +247,31 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int* ids = reinterpret_cast<int*>(smem + L::off_ids);
       for (int item = pair; item < total; item += n_pairs) {
-        int t, sub_lo, sub_n, mb, nb;
+        int t, sub_lo, sub_n, mb, nb, expert = 0;
         item_coords<kNSub>(p, item, t, sub_lo, sub_n);
-        tile_coords(p, rank, ra.m_rot, t, mb, nb);
+        if constexpr (kMoE) {
+          moe_coords(p, ra, item, mb, nb, expert);
+        } else {
+          tile_coords(p, rank, ra.m_rot, t, mb, nb);
+        }
         const int row0 = mb * BM + cta_in_pair * 128;
-        if constexpr (kAG) {
+        if constexpr (kMoE) {
+          // dynamic mapping: this tile's rows are tokens [tok_lo, tok_hi] (sorted), gathered by id
+          const int* tb = ra.moe_tab + 4 + 3 * mb;
+          if (kAG && p.debug_mode != 1) ag_wait_rows(p, rank, tb[1], tb[2] + 1);
+          const int4* src = reinterpret_cast<const int4*>(ra.moe_rows + row0);
+#pragma unroll 4
+          for (int i = 0; i < 32; ++i) {
+            int4 v = src[i];
+            v.x = v.x >= 0 ? v.x / p.topk : p.M;   // padding rows read out of range -> zero-filled
+            v.y = v.y >= 0 ? v.y / p.topk : p.M;
+            v.z = v.z >= 0 ? v.z / p.topk : p.M;
+            v.w = v.w >= 0 ? v.w / p.topk : p.M;
+            reinterpret_cast<int4*>(ids)[i] = v;
+          }
+        } else if constexpr (kAG) {
           if (p.debug_mode != 1 && row0 < p.M) ag_wait_rows(p, rank, row0, min(row0 + 128, p.M));
         }
         // the sub-tile count is a compile-time constant inside the k-loop (hoisted branch)
@@ -250,7 +282,23 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
             uint8_t* sa = smem + L::off_a + stage * kAStage;
             uint8_t* sb = smem + L::off_b + stage * L::kBStage;
             const int kc = kb * kBK;
-            if constexpr (kPair == 2) {
+            if constexpr (kMoE) {
+#pragma unroll 4
+              for (int g = 0; g < 32; ++g) {
+                const int4 r4 = reinterpret_cast<const int4*>(ids)[g];
+                ptx::tma_gather4<kPair>(&ra.tm_a, &full[stage], sa + g * 512, kc, r4.x, r4.y, r4.z, r4.w);
+              }
+              if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) {
+                if constexpr (kPair == 2) {
+                  ptx::tma_load_4d<2>(&ra.tm_b0, &full[stage], sb, kc, nb * 128, cta_in_pair, expert);
+                } else {
+                  ptx::tma_load_4d<1>(&ra.tm_b0, &full[stage], sb, kc, nb * 128, 0, expert);
+                  ptx::tma_load_4d<1>(&ra.tm_b0, &full[stage], sb + 128 * 128, kc, nb * 128, 1, expert);
+                }
+              } else {
+                ptx::tma_load_3d<kPair>(&ra.tm_b0, &full[stage], sb, kc, nb * kUmmaN + cta_in_pair * 128, expert);
+              }
+            } else if constexpr (kPair == 2) {
               ptx::tma_load_2d_pair(&ra.tm_a, &full[stage], sa, kc, row0);
 #pragma unroll
               for (int q = 0; q < NS; ++q) {
@@ -369,9 +417,10 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     uint8_t* bufs = smem + L::off_epi + ew * 8192;
     int sbuf = 0, it = 0;
     for (int item = pair; item < total; item += n_pairs, ++it) {
-      int t, sub_lo, sub_n, mb, nb;
+      int t, sub_lo, sub_n, mb, nb, expert;
       item_coords<kNSub>(p, item, t, sub_lo, sub_n);
-      tile_coords(p, rank, ra.m_rot, t, mb, nb);
+      if constexpr (kMoE) moe_coords(p, ra, item, mb, nb, expert);
+      else tile_coords(p, rank, ra.m_rot, t, mb, nb);
       const int as = it % kAccBufs;
       ptx::mbar_wait(&tfull[as], (it / kAccBufs) & 1);
       ptx::tc_fence_after();
@@ -498,6 +547,109 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kPair>(tmem_base, 512);
+  }
+}
+
+// Dynamic tile-centric mapping for the MoE first half ("lookup tables, whose values can
+// be filled at runtime ... by other dynamic logics (e.g., dynamic routing)").  One CTA of 1024
+// threads builds, from topk_ids [M, topk]:
+//   offs[E+1]   padded group starts (each expert's routed rows padded to a multiple of BM),
+//   rows[g]     token*topk + k of grouped row g, sorted stably by (expert, token); -1 for padding,
+//   tab         {n_tiles, 0, 0, 0, then per tile: expert, first token, last token}  (f_S, f_R inputs),
+//   sched[j]    tiles ordered by the producer tile their last token lives in (expected arrival).
+// Every rank builds identical tables from the identical routing: no communication.
+constexpr int kMoeThreads = 1024;
+__global__ void __launch_bounds__(kMoeThreads, 1)
+    tl_moe_tables_kernel(const int* __restrict__ ids, int n, int topk, int E, int BM, int M_r, int Tm, int* rows,
+                         int* offs, int* tab, int* sched, int max_tiles, int* err) {
+  extern __shared__ int sh[];
+  int* cnt = sh;                 // [E]
+  int* base = cnt + E;           // [E]
+  int* wcnt = base + E;          // [32][E]
+  int* wpre = wcnt + 32 * E;     // [32][E]
+  int* soffs = wpre + 32 * E;    // [E + 1]
+  int* keys = soffs + E + 1;     // [max_tiles]
+  int* bcnt = keys + max_tiles;  // [kMoeThreads] bucket counts -> starts
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < E; e += kMoeThreads) cnt[e] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += kMoeThreads) {
+    const int e = ids[i];
+    if (e < 0 || e >= E) atomicExch(err, 1);
+    else atomicAdd(&cnt[e], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int o = 0;
+    for (int e = 0; e < E; ++e) {
+      soffs[e] = o;
+      o += (cnt[e] + BM - 1) / BM * BM;
+    }
+    soffs[E] = o;
+    tab[0] = o / BM;
+  }
+  __syncthreads();
+  for (int e = tid; e <= E; e += kMoeThreads) offs[e] = soffs[e];
+  for (int e = tid; e < E; e += kMoeThreads) base[e] = soffs[e];
+  // stable counting sort: blocks of 1024 entries in order; rank inside a warp by __match_any,
+  // warp offsets by a per-expert scan over the 32 warps, expert bases carried across blocks
+  for (int b0 = 0; b0 < n; b0 += kMoeThreads) {
+    for (int x = tid; x < 32 * E; x += kMoeThreads) wcnt[x] = 0;
+    __syncthreads();
+    const int i = b0 + tid;
+    int e = i < n ? ids[i] : -1;
+    if (e >= E) e = -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int lrank = __popc(peers & ((1u << lane) - 1u));
+    if (e >= 0 && lrank == 0) wcnt[warp * E + e] = __popc(peers);
+    __syncthreads();
+    for (int x = tid; x < E; x += kMoeThreads) {
+      int run = base[x];
+      for (int w = 0; w < 32; ++w) {
+        wpre[w * E + x] = run;
+        run += wcnt[w * E + x];
+      }
+      base[x] = run;
+    }
+    __syncthreads();
+    if (e >= 0) rows[wpre[warp * E + e] + lrank] = i;
+    __syncthreads();
+  }
+  for (int e = 0; e < E; ++e)
+    for (int g = soffs[e] + cnt[e] + tid; g < soffs[e + 1]; g += kMoeThreads) rows[g] = -1;
+  __syncthreads();
+  const int n_tiles = soffs[E] / BM;
+  const int n_buckets = min((M_r + Tm - 1) / Tm, kMoeThreads);
+  for (int x = tid; x < kMoeThreads; x += kMoeThreads) bcnt[x] = 0;
+  __syncthreads();
+  for (int t = tid; t < n_tiles; t += kMoeThreads) {
+    const int g0 = t * BM;
+    int e = 0;
+    while (soffs[e + 1] <= g0) ++e;
+    const int last = min(g0 + BM, soffs[e] + cnt[e]) - 1;
+    const int lo = rows[g0] / topk, hi = rows[last] / topk;
+    tab[4 + 3 * t] = e;
+    tab[5 + 3 * t] = lo;
+    tab[6 + 3 * t] = hi;
+    // key: the producer tile (arrival slot) of the latest row this tile needs
+    const int key = (lo / M_r == hi / M_r) ? (hi % M_r) / Tm : (M_r - 1) / Tm;
+    keys[t] = min(key, n_buckets - 1);
+    atomicAdd(&bcnt[keys[t]], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int o = 0;
+    for (int b = 0; b < n_buckets; ++b) {
+      const int c = bcnt[b];
+      bcnt[b] = o;
+      o += c;
+    }
+  }
+  __syncthreads();
+  if (tid < n_buckets) {
+    int o = bcnt[tid];
+    for (int t = 0; t < n_tiles; ++t)
+      if (keys[t] == tid) sched[o++] = t;
   }
 }
 

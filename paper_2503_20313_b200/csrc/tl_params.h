@@ -26,6 +26,11 @@ struct alignas(64) RankArgs {
   const uint8_t* a_shard;  // AG copy source: this rank's [M/world, K] shard
   int rank;
   int m_rot;          // first schedule m-block (ORDER_ROTATE)
+  // MoE (dynamic mapping): grouped-row -> token*topk + k (-1 = padding), tile table
+  // {n_tiles, -, -, -, then per tile: expert, first token, last token} and the tile schedule
+  const int* moe_rows;
+  const int* moe_tab;
+  const int* moe_sched;
 };
 
 struct alignas(64) Params {
@@ -51,6 +56,7 @@ struct alignas(64) Params {
   // overlap-ratio measurement: 0 = normal, 1 = computation only (no AG copies or waits,
   // A read from whatever X_full holds), 2 = communication only (only the AG copy role runs)
   int debug_mode;
+  int topk;           // MoE: routed slots per token
 };
 
 }  // namespace tl
