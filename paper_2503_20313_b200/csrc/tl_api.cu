@@ -258,8 +258,15 @@ tl_status launch_t(tl_comm* c, const Params& p, cudaStream_t stream) {
   return TL_OK;
 }
 
-tl_status launch_moe(tl_comm* c, const Params& p, int epi, bool ag, cudaStream_t s) {
+tl_status launch_moe(tl_comm* c, const Params& p, int epi, bool ag, int nsub, cudaStream_t s) {
   const int pair = pair_of(c);
+  if (pair == 2 && nsub == 2) {
+    if (epi == EPI_STORE)
+      return ag ? launch_t<2, EPI_STORE, true, 2, true>(c, p, s) : launch_t<2, EPI_STORE, false, 2, true>(c, p, s);
+    if (epi == EPI_SILU_MUL)
+      return ag ? launch_t<2, EPI_SILU_MUL, true, 2, true>(c, p, s) : launch_t<2, EPI_SILU_MUL, false, 2, true>(c, p, s);
+    return ag ? launch_t<2, EPI_GELU_MUL, true, 2, true>(c, p, s) : launch_t<2, EPI_GELU_MUL, false, 2, true>(c, p, s);
+  }
   if (pair == 2) {
     if (epi == EPI_STORE)
       return ag ? launch_t<2, EPI_STORE, true, 1, true>(c, p, s) : launch_t<2, EPI_STORE, false, 1, true>(c, p, s);
@@ -435,11 +442,15 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   p.M_r = (int)M_r;
   p.epoch = epoch;
   p.m_blocks = (int)((M + 128 * pair - 1) / (128 * pair));
-  const int nsub = moe ? 1 : choose_nsub(c, M, N_out, K, act != TL_ACT_NONE);
+  // MoE: 512-wide tiles whenever N fills them -- one gathered A stage then feeds twice the MMAs
+  const int nsub = moe ? ((pair_of(c) == 2 && c->opt.n_sub != 1 &&
+                           (c->opt.n_sub == 2 || N_out >= (act != TL_ACT_NONE ? 256 : 512))) ? 2 : 1)
+                       : choose_nsub(c, M, N_out, K, act != TL_ACT_NONE);
   const int bn_out = (act ? 128 : 256) * nsub;
   p.n_blocks = (int)((N_out + bn_out - 1) / bn_out);
   p.k_blocks = (int)((K + kBK - 1) / kBK);
   set_items(p, nsub, p.ctas_per_rank / pair);
+  if (moe) p.n_full = 1 << 30;   // MoE tiles are always whole (the tile count is data dependent)
   p.tm_rows = sm.Tm;
   p.tiles_per_rank = sm.tiles_per_rank;
   p.tiles_per_channel = sm.tiles_per_channel;
@@ -562,7 +573,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   }
   if (st == TL_OK) {
     const int epi = act == TL_ACT_NONE ? EPI_STORE : act == TL_ACT_SILU_MUL ? EPI_SILU_MUL : EPI_GELU_MUL;
-    st = moe ? launch_moe(c, p, epi, comm, stream) : launch(c, p, epi, comm, nsub, stream);
+    st = moe ? launch_moe(c, p, epi, comm, nsub, stream) : launch(c, p, epi, comm, nsub, stream);
   }
   if (st == TL_OK && dma) {  // join: later work on `stream` is ordered after every copy
     cudaError_t e = cudaSuccess;

@@ -242,36 +242,82 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  // MoE producer: the 32 row gathers (tile::gather4) of every k-block are issued by two threads
+  // (warp 0 lane 0: gathers 0-15 + the expert's B tile + the barrier arm; warp 2 lane 0: gathers
+  // 16-31), so the per-instruction issue cost of the gathers does not starve the tensor cores.
+  constexpr int kGPer = kAG ? 16 : 11;   // gathers per issuer: 2 issuers (AG: warp 3 copies) or 3
+  auto moe_produce = [&](bool is_main, int g0) {
+    int stage = 0;
+    uint32_t phase = 0;
+    const int ng = min(kGPer, 32 - g0);
+    int4 ids4[kGPer];
+    for (int item = pair; item < total; item += n_pairs) {
+      int mb, nb, expert;
+      moe_coords(p, ra, item, mb, nb, expert);
+      const int row0 = mb * BM + cta_in_pair * 128;
+      // dynamic mapping: this tile's rows are tokens [tok_lo, tok_hi] (sorted), gathered by id
+      const int* tb = ra.moe_tab + 4 + 3 * mb;
+      if (kAG && p.debug_mode != 1) ag_wait_rows(p, rank, tb[1], tb[2] + 1);
+      const int4* src = reinterpret_cast<const int4*>(ra.moe_rows + row0) + g0;
+#pragma unroll
+      for (int i = 0; i < kGPer; ++i) {
+        int4 v = i < ng ? src[i] : make_int4(0, 0, 0, 0);
+        v.x = v.x >= 0 ? v.x / p.topk : p.M;   // padding rows read out of range -> zero-filled
+        v.y = v.y >= 0 ? v.y / p.topk : p.M;
+        v.z = v.z >= 0 ? v.z / p.topk : p.M;
+        v.w = v.w >= 0 ? v.w / p.topk : p.M;
+        ids4[i] = v;
+      }
+      for (int kb = 0; kb < p.k_blocks; ++kb) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + L::off_a + stage * kAStage;
+        uint8_t* sb = smem + L::off_b + stage * L::kBStage;
+        const int kc = kb * kBK;
+#pragma unroll
+        for (int i = 0; i < kGPer; ++i)
+          if (i < ng)
+            ptx::tma_gather4<kPair>(&ra.tm_a, &full[stage], sa + (g0 + i) * 512, kc, ids4[i].x, ids4[i].y, ids4[i].z,
+                                    ids4[i].w);
+        if (is_main) {
+#pragma unroll
+          for (int sub = 0; sub < kNSub; ++sub) {   // one gathered A stage feeds kNSub 256-wide sub-tiles
+            uint8_t* sbs = sb + sub * L::kBBox;
+            if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) {
+              const int nrow = nb * 128 * kNSub + sub * 128;
+              if constexpr (kPair == 2) {
+                ptx::tma_load_4d<2>(&ra.tm_b0, &full[stage], sbs, kc, nrow, cta_in_pair, expert);
+              } else {
+                ptx::tma_load_4d<1>(&ra.tm_b0, &full[stage], sbs, kc, nrow, 0, expert);
+                ptx::tma_load_4d<1>(&ra.tm_b0, &full[stage], sbs + 128 * 128, kc, nrow, 1, expert);
+              }
+            } else {
+              ptx::tma_load_3d<kPair>(&ra.tm_b0, &full[stage], sbs, kc, nb * kAccCols + sub * kUmmaN + cta_in_pair * 128,
+                                      expert);
+            }
+          }
+          if (cta_in_pair == 0)
+            ptx::mbar_arrive_expect_tx(&full[stage], (kAStage + kNSub * L::kBBox) * kPair);
+          else
+            ptx::mbar_arrive_cluster(&full[stage], 0);
+        }
+        if (++stage == kStages) stage = 0, phase ^= 1;
+      }
+    }
+  };
+
+  if (kMoE && (warp == 0 || warp == 2 || (!kAG && warp == 3))) {
+    if (lane == 0) moe_produce(warp == 0, warp == 0 ? 0 : warp == 2 ? kGPer : 2 * kGPer);
+  } else if (warp == 0) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int* ids = reinterpret_cast<int*>(smem + L::off_ids);
       for (int item = pair; item < total; item += n_pairs) {
-        int t, sub_lo, sub_n, mb, nb, expert = 0;
+        int t, sub_lo, sub_n, mb, nb;
         item_coords<kNSub>(p, item, t, sub_lo, sub_n);
-        if constexpr (kMoE) {
-          moe_coords(p, ra, item, mb, nb, expert);
-        } else {
-          tile_coords(p, rank, ra.m_rot, t, mb, nb);
-        }
+        tile_coords(p, rank, ra.m_rot, t, mb, nb);
         const int row0 = mb * BM + cta_in_pair * 128;
-        if constexpr (kMoE) {
-          // dynamic mapping: this tile's rows are tokens [tok_lo, tok_hi] (sorted), gathered by id
-          const int* tb = ra.moe_tab + 4 + 3 * mb;
-          if (kAG && p.debug_mode != 1) ag_wait_rows(p, rank, tb[1], tb[2] + 1);
-          const int4* src = reinterpret_cast<const int4*>(ra.moe_rows + row0);
-#pragma unroll 4
-          for (int i = 0; i < 32; ++i) {
-            int4 v = src[i];
-            v.x = v.x >= 0 ? v.x / p.topk : p.M;   // padding rows read out of range -> zero-filled
-            v.y = v.y >= 0 ? v.y / p.topk : p.M;
-            v.z = v.z >= 0 ? v.z / p.topk : p.M;
-            v.w = v.w >= 0 ? v.w / p.topk : p.M;
-            reinterpret_cast<int4*>(ids)[i] = v;
-          }
-        } else if constexpr (kAG) {
+        if constexpr (kAG) {
           if (p.debug_mode != 1 && row0 < p.M) ag_wait_rows(p, rank, row0, min(row0 + 128, p.M));
         }
         // the sub-tile count is a compile-time constant inside the k-loop (hoisted branch)
@@ -282,23 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
             uint8_t* sa = smem + L::off_a + stage * kAStage;
             uint8_t* sb = smem + L::off_b + stage * L::kBStage;
             const int kc = kb * kBK;
-            if constexpr (kMoE) {
-#pragma unroll 4
-              for (int g = 0; g < 32; ++g) {
-                const int4 r4 = reinterpret_cast<const int4*>(ids)[g];
-                ptx::tma_gather4<kPair>(&ra.tm_a, &full[stage], sa + g * 512, kc, r4.x, r4.y, r4.z, r4.w);
-              }
-              if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) {
-                if constexpr (kPair == 2) {
-                  ptx::tma_load_4d<2>(&ra.tm_b0, &full[stage], sb, kc, nb * 128, cta_in_pair, expert);
-                } else {
-                  ptx::tma_load_4d<1>(&ra.tm_b0, &full[stage], sb, kc, nb * 128, 0, expert);
-                  ptx::tma_load_4d<1>(&ra.tm_b0, &full[stage], sb + 128 * 128, kc, nb * 128, 1, expert);
-                }
-              } else {
-                ptx::tma_load_3d<kPair>(&ra.tm_b0, &full[stage], sb, kc, nb * kUmmaN + cta_in_pair * 128, expert);
-              }
-            } else if constexpr (kPair == 2) {
+            if constexpr (kPair == 2) {
               ptx::tma_load_2d_pair(&ra.tm_a, &full[stage], sa, kc, row0);
 #pragma unroll
               for (int q = 0; q < NS; ++q) {

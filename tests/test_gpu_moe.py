@@ -20,7 +20,7 @@ def tl():
     return m
 
 
-def _run(tl, W, M, H, E, topk, N_out, act, skew=0.0, pair=2, placement=False, seed=0):
+def _run(tl, W, M, H, E, topk, N_out, act, skew=0.0, pair=2, placement=False, seed=0, nsub=0):
     N1 = N_out * (1 if act == TI.ACT_NONE else 2)
     if placement:
         Xs, Ws = TI.moe_placement_inputs(M, H, E, N1, W)
@@ -31,6 +31,7 @@ def _run(tl, W, M, H, E, topk, N_out, act, skew=0.0, pair=2, placement=False, se
     ids = TI.moe_routing(M, E, topk, seed=seed + 2, skew=skew)
     comm = tl.Comm.loopback(W, 0, max_M=M, max_H=H) if W > 1 else tl.Comm.single(0, max_M=M, max_H=H)
     comm.set_option("cta_pair", pair)
+    comm.set_option("n_sub", nsub)
     R = tl.moe_capacity(comm, M, topk, E)
     Ys = [torch.empty(R, N_out, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
     rows = [torch.empty(R, device="cuda", dtype=torch.int32) for _ in range(W)]
@@ -66,14 +67,15 @@ def _check(ref_rows, ref_Y, Ys, rows, offs, topk, exact=False):
 
 @pytest.mark.parametrize("W", [1, 2, 4, 8])
 @pytest.mark.parametrize("act", [TI.ACT_NONE, TI.ACT_SILU_MUL])
-def test_moe_parity(tl, W, act):
-    res = _run(tl, W, M=256 * W if W > 1 else 512, H=192, E=8, topk=2, N_out=192, act=act)
+@pytest.mark.parametrize("nsub", [1, 2])
+def test_moe_parity(tl, W, act, nsub):
+    res = _run(tl, W, M=256 * W if W > 1 else 512, H=192, E=8, topk=2, N_out=320, act=act, nsub=nsub)
     _check(*res)
 
 
-@pytest.mark.parametrize("pair", [1, 2])
-def test_moe_placement_bit_exact(tl, pair):
-    res = _run(tl, 4, M=512, H=64, E=6, topk=3, N_out=96, act=TI.ACT_NONE, placement=True, pair=pair)
+@pytest.mark.parametrize("pair,nsub", [(1, 1), (2, 1), (2, 2)])
+def test_moe_placement_bit_exact(tl, pair, nsub):
+    res = _run(tl, 4, M=512, H=64, E=6, topk=3, N_out=520, act=TI.ACT_NONE, placement=True, pair=pair, nsub=nsub)
     _check(*res, exact=True)
 
 
