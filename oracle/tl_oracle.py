@@ -239,3 +239,29 @@ def moe_ag_group_gemm(X_shards, topk_ids, W1_list, act: int):
             np.zeros((0, W1.shape[1] // (1 if act == ACT_NONE else 2)))
         Ys.append(Y)
     return rows, Ys
+
+
+# ----------------------------------------------------------------------------
+# MoE second half: GroupGEMM + Scatter + TopK reduce + ReduceScatter
+# ----------------------------------------------------------------------------
+def moe_group_gemm_rs(rows, Zg_list, W2_list, topk_weights, M: int):
+    """P:632/P:647 second part: P_s[j] = Zg_s[j] . W2_s[e_j]^T for every grouped row j = (e, t, k);
+    scatter back to the token and reduce over its top-k slots with the router weights,
+    Q_s[t] = sum_k w[t, k] P_s[j(t, k)]; then ReduceScatter over ranks: out_r = sum_s Q_s[rows of r]."""
+    w = np.asarray(topk_weights, dtype=np.float64)
+    Qs = []
+    for Zg, W2 in zip(Zg_list, W2_list):
+        Zg = np.asarray(Zg, dtype=np.float64)
+        W2 = np.asarray(W2, dtype=np.float64)
+        Q = np.zeros((M, W2.shape[1]))
+        for j, (e, t, k) in enumerate(rows):   # scatter + top-k reduce, in grouped order
+            Q[t] += w[t, k] * (Zg[j] @ W2[e].T)
+        Qs.append(Q)
+    return reduce_scatter_rows(Qs)
+
+
+def moe_forward(X_shards, topk_ids, topk_weights, W1_list, W2_list, act: int):
+    """TP MoE FFN: AG + Gather + GroupGEMM + act, then GroupGEMM + Scatter + TopK reduce + RS."""
+    rows, Zs = moe_ag_group_gemm(X_shards, topk_ids, W1_list, act)
+    M = sum(np.asarray(x).shape[0] for x in X_shards)
+    return moe_group_gemm_rs(rows, Zs, W2_list, topk_weights, M)

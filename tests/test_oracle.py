@@ -271,3 +271,41 @@ def test_moe_pyloop_and_placement_closed_form():
     for j, (e, t, k) in enumerate(rows):
         for n in range(N1):
             assert sum(a * b for a, b in zip(X[t], W1[e][n])) == Ys[1][j, n]
+
+
+def test_moe_single_expert_is_dense_mlp():
+    """E = 1, top-1, weight 1: the TP MoE FFN is exactly the dense TP MLP."""
+    W, M, H, I = 2, 16, 8, 12
+    X, G, U, W2 = TI.mlp_full(M, H, I, seed=6)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    f = lambda L: [TI.to_f64(t) for t in L]
+    ids = np.zeros((M, 1), dtype=np.int64)
+    w = np.ones((M, 1))
+    outs = O.moe_forward(f(Xs), ids, w, [x[None] for x in f(W1s)], [x[None] for x in f(W2s)], TI.ACT_SILU_MUL)
+    ref = O.mlp_forward(f(Xs), f(W1s), f(W2s), TI.ACT_SILU_MUL)
+    for r in range(W):
+        np.testing.assert_allclose(outs[r], ref[r], rtol=1e-12, atol=1e-12)
+
+
+def test_moe_second_half_closed_form_and_brute_force():
+    # all-ones Zg and W2, weights summing to 1 per token: every output = W * I_l (S:347 analogue)
+    W, M, H, E, topk, Il = 2, 8, 4, 3, 2, 5
+    ids = TI.moe_routing(M, E, topk, seed=1).numpy()
+    rows = O.moe_group_rows(ids, E)
+    w = TI.moe_topk_weights(M, topk, seed=2).double().numpy()
+    Zg = [np.ones((len(rows), Il)) for _ in range(W)]
+    W2 = [np.ones((E, H, Il)) for _ in range(W)]
+    outs = O.moe_group_gemm_rs(rows, Zg, W2, w, M)
+    np.testing.assert_allclose(np.concatenate(outs), W * Il, rtol=1e-14)
+    # brute force on random data, per token, pure Python sums
+    Zg = [np.random.default_rng(3 + r).standard_normal((len(rows), Il)) for r in range(W)]
+    W2 = [np.random.default_rng(9 + r).standard_normal((E, H, Il)) for r in range(W)]
+    outs = O.moe_group_gemm_rs(rows, Zg, W2, w, M)
+    for t in range(M):
+        for h in range(H):
+            ref = 0.0
+            for r in range(W):
+                for j, (e, tt, k) in enumerate(rows):
+                    if tt == t:
+                        ref += w[t, k] * sum(Zg[r][j, i] * W2[r][e, h, i] for i in range(Il))
+            assert abs(outs[t // (M // W)][t % (M // W), h] - ref) < 1e-12

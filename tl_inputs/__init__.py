@@ -176,3 +176,15 @@ def moe_placement_inputs(M: int, H: int, E: int, N1: int, W: int):
                     B[e, n, 4 * q + j] = float(1 << j)
         Ws.append(B.to(torch.bfloat16))
     return shard_rows(X.to(torch.bfloat16), W), Ws
+
+
+def moe_topk_weights(M: int, topk: int, seed: int = 0):
+    """Router weights: a seeded softmax-like positive row of topk values summing to 1, fp32 [M, topk]."""
+    g = torch.Generator().manual_seed(int(seed) * 1000 + 9)
+    w = torch.rand(M, topk, generator=g, dtype=torch.float32) + 0.1
+    return (w / w.sum(1, keepdim=True)).contiguous()
+
+
+def moe_down_weights(E: int, H: int, I_l: int, W: int, seed: int = 0):
+    """Per-rank expert down projections [E, H, I_l] bf16 ~ N(0, 1/(W * I_l))."""
+    return [_randn((E, H, I_l), seed + 19 * r, _TID_W2, (W * I_l) ** -0.5) for r in range(W)]
