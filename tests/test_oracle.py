@@ -293,6 +293,7 @@ def test_moe_second_half_closed_form_and_brute_force():
     ids = TI.moe_routing(M, E, topk, seed=1).numpy()
     rows = O.moe_group_rows(ids, E)
     w = TI.moe_topk_weights(M, topk, seed=2).double().numpy()
+    w = w / w.sum(1, keepdims=True)          # exactly 1 per token in fp64
     Zg = [np.ones((len(rows), Il)) for _ in range(W)]
     W2 = [np.ones((E, H, Il)) for _ in range(W)]
     outs = O.moe_group_gemm_rs(rows, Zg, W2, w, M)
