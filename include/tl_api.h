@@ -83,6 +83,12 @@ const char* tl_build_info(void);       /* compile target + version string */
  *   tl_comm_create_loopback(world, device, caps, &c)  -- ready to use, no connect.
  * Capacities: max_M = largest global M, max_H = largest AG width K (= H) and RS width N (= H). */
 size_t tl_handle_size(void);
+/* _ex variants: max_topk sizes the reduce-scatter staging for the MoE second half
+ * ([world][max_M/world][max_topk][max_H] per bank); the plain variants use max_topk = 1. */
+tl_status tl_comm_create_ex(int rank, int world, int device, int64_t max_M, int64_t max_H, int max_topk,
+                            void* my_handle, tl_comm_t* out);
+tl_status tl_comm_create_loopback_ex(int world, int device, int64_t max_M, int64_t max_H, int max_topk,
+                                     tl_comm_t* out);
 tl_status tl_comm_create(int rank, int world, int device, int64_t max_M, int64_t max_H,
                          void* my_handle, tl_comm_t* out);
 tl_status tl_comm_connect(tl_comm_t comm, const void* all_handles);
@@ -120,7 +126,8 @@ tl_status tl_get_option(tl_comm_t comm, const char* key, int64_t* value);
 
 /* Synchronises the device, then returns TL_OK or TL_ERR_TIMEOUT and fills
  * diag_out[0..7] = {status, rank, kind (1 = AG wait, 2 = RS wait), src rank, index,
- * observed, expected, epoch} of the first timed-out wait (zeros if none).  Clears the record. */
+ * observed, expected, epoch} of the first timed-out wait (zeros if none; kind 3 = MoE owner
+ * reduce wait).  Clears the record. */
 tl_status tl_comm_check(tl_comm_t comm, int64_t diag_out[8]);
 
 /* ---------------------------------------------------------------- the three ops -----------
@@ -193,6 +200,23 @@ tl_status tl_moe_ag_gemm_loopback(tl_comm_t comm, const void* const* X_shard,
                                   const int32_t* const* topk_ids, const void* const* W1, void* const* Y,
                                   int32_t* const* row_ids, int32_t* const* expert_offsets, int64_t M,
                                   int64_t H, int64_t N_out, int E, int topk, tl_act act, void* stream);
+
+/* MoE second half: GroupGEMM + Scatter + TopK reduce + ReduceScatter:
+ *   out_shard[t - r*M/world, :] = sum_s sum_k w[t, k] * ( Zg_s[g(t, k)] . W2_s[e(t, k)]^T )
+ * for the tokens t of rank r, where g(t, k) is the grouped row of (t, k) given by row_ids /
+ * expert_offsets (as produced by tl_moe_ag_gemm) and s runs over ranks.
+ *   Zg bf16 [R_cap, I_local] (grouped rows), row_ids int32 [R_cap], expert_offsets int32 [E + 1],
+ *   topk_weights fp32 [M, topk] (router weights, identical on every rank), W2 bf16 [E, H, I_local],
+ *   out_shard bf16 [M/world, H].  Needs topk <= the comm's max_topk.  The grouped GEMM's epilogue
+ *   scatters w * row to the owner's staging slot [src rank][token][k] (NVLink stores); the last CTA
+ *   of each rank releases that rank's slot flag on every owner; an owner kernel sums in fp32. */
+tl_status tl_moe_gemm_rs(tl_comm_t comm, const void* Zg, const int32_t* row_ids, const int32_t* expert_offsets,
+                         const float* topk_weights, const void* W2, void* out_shard, int64_t M, int64_t H,
+                         int64_t I_local, int E, int topk, void* stream);
+tl_status tl_moe_gemm_rs_loopback(tl_comm_t comm, const void* const* Zg, const int32_t* const* row_ids,
+                                  const int32_t* const* expert_offsets, const float* const* topk_weights,
+                                  const void* const* W2, void* const* out_shard, int64_t M, int64_t H,
+                                  int64_t I_local, int E, int topk, void* stream);
 
 /* ---------------------------------------------------------------- diagnostics -------------
  * Evaluates the device-side static mapping for producer tiles t = 0..n-1 of a

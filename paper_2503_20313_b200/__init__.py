@@ -15,7 +15,7 @@ ACT_NONE, ACT_SILU_MUL, ACT_GELU_TANH_MUL = 0, 1, 2
 ACTS = {"none": ACT_NONE, "silu_mul": ACT_SILU_MUL, "gelu_tanh_mul": ACT_GELU_TANH_MUL}
 
 __all__ = ["Comm", "TLError", "lib", "ACT_NONE", "ACT_SILU_MUL", "ACT_GELU_TANH_MUL", "static_map_device",
-           "moe_capacity", "moe_ag_gemm", "moe_ag_gemm_lb"]
+           "moe_capacity", "moe_ag_gemm", "moe_ag_gemm_lb", "moe_gemm_rs", "moe_gemm_rs_lb"]
 
 
 def _ptr(t):
@@ -44,24 +44,26 @@ class Comm:
 
     # ------------------------------------------------------------------ construction
     @classmethod
-    def loopback(cls, world: int, device: int = 0, max_M: int = 8192, max_H: int = 4096):
+    def loopback(cls, world: int, device: int = 0, max_M: int = 8192, max_H: int = 4096, max_topk: int = 1):
         """All `world` ranks emulated on one device, driven by single launches."""
         L = lib()
         h = C.c_void_p()
-        check(L.tl_comm_create_loopback(world, device, max_M, max_H, C.byref(h)), "tl_comm_create_loopback")
+        check(L.tl_comm_create_loopback_ex(world, device, max_M, max_H, max_topk, C.byref(h)),
+              "tl_comm_create_loopback_ex")
         return cls(h.value, -1, world, world, device)
 
     @classmethod
-    def single(cls, device: int = 0, max_M: int = 8192, max_H: int = 4096):
+    def single(cls, device: int = 0, max_M: int = 8192, max_H: int = 4096, max_topk: int = 1):
         """World of one rank (AG/RS degenerate to identities)."""
         L = lib()
         h = C.c_void_p()
         buf = C.create_string_buffer(L.tl_handle_size())
-        check(L.tl_comm_create(0, 1, device, max_M, max_H, buf, C.byref(h)), "tl_comm_create")
+        check(L.tl_comm_create_ex(0, 1, device, max_M, max_H, max_topk, buf, C.byref(h)), "tl_comm_create_ex")
         return cls(h.value, 0, 1, 1, device)
 
     @classmethod
-    def from_process_group(cls, group=None, device: int | None = None, max_M: int = 8192, max_H: int = 4096):
+    def from_process_group(cls, group=None, device: int | None = None, max_M: int = 8192, max_H: int = 4096,
+                           max_topk: int = 1):
         """One process per GPU: create, all-gather the IPC handles over `group`, connect."""
         import torch
         import torch.distributed as dist
@@ -72,7 +74,7 @@ class Comm:
             device = torch.cuda.current_device()
         h = C.c_void_p()
         buf = C.create_string_buffer(L.tl_handle_size())
-        check(L.tl_comm_create(rank, world, device, max_M, max_H, buf, C.byref(h)), "tl_comm_create")
+        check(L.tl_comm_create_ex(rank, world, device, max_M, max_H, max_topk, buf, C.byref(h)), "tl_comm_create_ex")
         comm = cls(h.value, rank, world, 1, device)
         if world > 1:
             allh = exchange_handles(bytes(buf.raw), group)
@@ -192,6 +194,24 @@ def moe_ag_gemm_lb(comm, X_shards, topk_ids, W1s, Ys, row_ids, offsets, act: int
     check(lib().tl_moe_ag_gemm_loopback(comm._h, *[a[0] for a in arrs], M, H, N_out, E, topk, act,
                                         _stream(stream)), "tl_moe_ag_gemm_loopback")
     return Ys
+
+
+def moe_gemm_rs(comm, Zg, row_ids, offsets, topk_weights, W2, out_shard, stream=None):
+    """MoE GroupGEMM + Scatter + TopK reduce + RS on a one-rank-per-process comm (see tl_api.h)."""
+    M, topk = topk_weights.shape
+    E, H, I_l = W2.shape
+    check(lib().tl_moe_gemm_rs(comm._h, _ptr(Zg), _ptr(row_ids), _ptr(offsets), _ptr(topk_weights), _ptr(W2),
+                               _ptr(out_shard), M, H, I_l, E, topk, _stream(stream)), "tl_moe_gemm_rs")
+    return out_shard
+
+
+def moe_gemm_rs_lb(comm, Zgs, row_ids, offsets, topk_weights, W2s, outs, stream=None):
+    M, topk = topk_weights[0].shape
+    E, H, I_l = W2s[0].shape
+    arrs = [ptr_array([_ptr(t) for t in L]) for L in (Zgs, row_ids, offsets, topk_weights, W2s, outs)]
+    check(lib().tl_moe_gemm_rs_loopback(comm._h, *[a[0] for a in arrs], M, H, I_l, E, topk, _stream(stream)),
+          "tl_moe_gemm_rs_loopback")
+    return outs
 
 
 def static_map_device(M: int, world: int, tm_rows: int, channels_per_rank: int, n: int):

@@ -36,6 +36,10 @@ SIGNATURES = {
     "tl_mlp_forward_loopback": (_int, [_vp, _vpp, _vpp, _vpp, _vpp, _vpp, _i64, _i64, _i64, _int, _vp]),
     "tl_debug_static_map": (_int, [_i64, _int, _i64, _int, _i64, C.POINTER(_i64)]),
     "tl_moe_capacity": (_i64, [_vp, _i64, _int, _int]),
+    "tl_comm_create_ex": (_int, [_int, _int, _int, _i64, _i64, _int, _vp, C.POINTER(_vp)]),
+    "tl_comm_create_loopback_ex": (_int, [_int, _int, _i64, _i64, _int, C.POINTER(_vp)]),
+    "tl_moe_gemm_rs": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp]),
+    "tl_moe_gemm_rs_loopback": (_int, [_vp, _vpp, _vpp, _vpp, _vpp, _vpp, _vpp, _i64, _i64, _i64, _int, _int, _vp]),
     "tl_moe_ag_gemm": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _int, _vp]),
     "tl_moe_ag_gemm_loopback": (_int, [_vp, _vpp, _vpp, _vpp, _vpp, _vpp, _vpp, _i64, _i64, _i64, _int, _int, _int,
                                        _vp]),

@@ -50,23 +50,25 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Handle {
   uint32_t magic, version;
   int32_t rank, world;
-  int64_t max_M, max_H;
+  int64_t max_M, max_H, max_topk;
   uint64_t ws_bytes;
   cudaIpcMemHandle_t ipc;
 };
 
 // Workspace layout of one rank (identical on every rank: symmetric).
 struct WsLayout {
-  size_t xfull[2], stage[2], ag_flags, rs_flags, diag, bytes;
-  static WsLayout make(int world, int64_t max_M, int64_t max_H) {
+  size_t xfull[2], stage[2], ag_flags, rs_flags, diag, moe_sync, bytes;
+  static WsLayout make(int world, int64_t max_M, int64_t max_H, int max_topk) {
     WsLayout l;
     const size_t xb = align_up((size_t)max_M * max_H * 2, kAlign);
+    const size_t sb = align_up((size_t)max_M * max_H * 2 * (size_t)max_topk, kAlign);
     size_t off = 0;
     for (int b = 0; b < 2; ++b) l.xfull[b] = off, off += xb;
-    for (int b = 0; b < 2; ++b) l.stage[b] = off, off += xb;   // [world][max_M/world][max_H]
+    for (int b = 0; b < 2; ++b) l.stage[b] = off, off += sb;   // [world][max_M/world][max_topk][max_H]
     l.ag_flags = off, off += align_up((size_t)world * kAgFlagStride * 4, kAlign);
     l.rs_flags = off, off += align_up((size_t)world * kRsFlagStride * 4, kAlign);
     l.diag = off, off += kAlign;
+    l.moe_sync = off, off += kAlign;   // MoE scatter: [world] slot flags at 0, CTA counter at 4096
     l.bytes = off;
     return l;
   }
@@ -169,6 +171,8 @@ struct tl_comm {
   int rank = -1, world = 1, n_local = 1, device = 0, sm_count = 148;
   bool loopback = false, connected = false;
   int64_t max_M = 0, max_H = 0;
+  int max_topk = 1;
+  unsigned moe_done = 0;            // CTA completions counted so far (identical on every rank)
   WsLayout lay{};
   uint8_t* ws[kMaxWorld] = {};      // workspace base of every rank (own, loopback-owned or IPC-mapped)
   bool owned[kMaxWorld] = {};       // cudaMalloc'd by us (else IPC-opened)
@@ -232,7 +236,7 @@ int ctas_per_rank(const tl_comm* c) {
   return n < pair ? pair : n;
 }
 
-template <int kPair, int kEpi, bool kAG, int kNSub, bool kMoE = false>
+template <int kPair, int kEpi, bool kAG, int kNSub, int kMoE = MOE_NONE>
 tl_status launch_t(tl_comm* c, const Params& p, cudaStream_t stream) {
   constexpr int kStages = stages_for(kPair, kAG, kNSub);
   using L = Layout<kPair, kStages, kAG, kNSub>;
@@ -261,24 +265,33 @@ tl_status launch_t(tl_comm* c, const Params& p, cudaStream_t stream) {
 tl_status launch_moe(tl_comm* c, const Params& p, int epi, bool ag, int nsub, cudaStream_t s) {
   const int pair = pair_of(c);
   if (pair == 2 && nsub == 2) {
+    if (epi == EPI_MOE_SCATTER) return launch_t<2, EPI_MOE_SCATTER, false, 2, MOE_SCATTER>(c, p, s);
     if (epi == EPI_STORE)
-      return ag ? launch_t<2, EPI_STORE, true, 2, true>(c, p, s) : launch_t<2, EPI_STORE, false, 2, true>(c, p, s);
+      return ag ? launch_t<2, EPI_STORE, true, 2, MOE_GATHER>(c, p, s) : launch_t<2, EPI_STORE, false, 2, MOE_GATHER>(c, p, s);
     if (epi == EPI_SILU_MUL)
-      return ag ? launch_t<2, EPI_SILU_MUL, true, 2, true>(c, p, s) : launch_t<2, EPI_SILU_MUL, false, 2, true>(c, p, s);
-    return ag ? launch_t<2, EPI_GELU_MUL, true, 2, true>(c, p, s) : launch_t<2, EPI_GELU_MUL, false, 2, true>(c, p, s);
+      return ag ? launch_t<2, EPI_SILU_MUL, true, 2, MOE_GATHER>(c, p, s)
+                : launch_t<2, EPI_SILU_MUL, false, 2, MOE_GATHER>(c, p, s);
+    return ag ? launch_t<2, EPI_GELU_MUL, true, 2, MOE_GATHER>(c, p, s)
+              : launch_t<2, EPI_GELU_MUL, false, 2, MOE_GATHER>(c, p, s);
   }
   if (pair == 2) {
+    if (epi == EPI_MOE_SCATTER) return launch_t<2, EPI_MOE_SCATTER, false, 1, MOE_SCATTER>(c, p, s);
     if (epi == EPI_STORE)
-      return ag ? launch_t<2, EPI_STORE, true, 1, true>(c, p, s) : launch_t<2, EPI_STORE, false, 1, true>(c, p, s);
+      return ag ? launch_t<2, EPI_STORE, true, 1, MOE_GATHER>(c, p, s) : launch_t<2, EPI_STORE, false, 1, MOE_GATHER>(c, p, s);
     if (epi == EPI_SILU_MUL)
-      return ag ? launch_t<2, EPI_SILU_MUL, true, 1, true>(c, p, s) : launch_t<2, EPI_SILU_MUL, false, 1, true>(c, p, s);
-    return ag ? launch_t<2, EPI_GELU_MUL, true, 1, true>(c, p, s) : launch_t<2, EPI_GELU_MUL, false, 1, true>(c, p, s);
+      return ag ? launch_t<2, EPI_SILU_MUL, true, 1, MOE_GATHER>(c, p, s)
+                : launch_t<2, EPI_SILU_MUL, false, 1, MOE_GATHER>(c, p, s);
+    return ag ? launch_t<2, EPI_GELU_MUL, true, 1, MOE_GATHER>(c, p, s)
+              : launch_t<2, EPI_GELU_MUL, false, 1, MOE_GATHER>(c, p, s);
   }
+  if (epi == EPI_MOE_SCATTER) return launch_t<1, EPI_MOE_SCATTER, false, 1, MOE_SCATTER>(c, p, s);
   if (epi == EPI_STORE)
-    return ag ? launch_t<1, EPI_STORE, true, 1, true>(c, p, s) : launch_t<1, EPI_STORE, false, 1, true>(c, p, s);
+    return ag ? launch_t<1, EPI_STORE, true, 1, MOE_GATHER>(c, p, s) : launch_t<1, EPI_STORE, false, 1, MOE_GATHER>(c, p, s);
   if (epi == EPI_SILU_MUL)
-    return ag ? launch_t<1, EPI_SILU_MUL, true, 1, true>(c, p, s) : launch_t<1, EPI_SILU_MUL, false, 1, true>(c, p, s);
-  return ag ? launch_t<1, EPI_GELU_MUL, true, 1, true>(c, p, s) : launch_t<1, EPI_GELU_MUL, false, 1, true>(c, p, s);
+    return ag ? launch_t<1, EPI_SILU_MUL, true, 1, MOE_GATHER>(c, p, s)
+              : launch_t<1, EPI_SILU_MUL, false, 1, MOE_GATHER>(c, p, s);
+  return ag ? launch_t<1, EPI_GELU_MUL, true, 1, MOE_GATHER>(c, p, s)
+            : launch_t<1, EPI_GELU_MUL, false, 1, MOE_GATHER>(c, p, s);
 }
 
 tl_status launch(tl_comm* c, const Params& p, int epi, bool ag, int nsub, cudaStream_t s) {
@@ -723,9 +736,9 @@ tl_status alloc_ws(tl_comm* c, int r) {
   return TL_OK;
 }
 
-tl_status init_common(tl_comm* c, int world, int device, int64_t max_M, int64_t max_H) {
+tl_status init_common(tl_comm* c, int world, int device, int64_t max_M, int64_t max_H, int max_topk) {
   if (world < 1 || world > kMaxWorld) return fail(TL_ERR_UNSUPPORTED, "world must be in [1, %d]", kMaxWorld);
-  if (max_M < 1 || max_H < 8) return fail(TL_ERR_INVALID, "bad capacities");
+  if (max_M < 1 || max_H < 8 || max_topk < 1 || max_topk > 64) return fail(TL_ERR_INVALID, "bad capacities");
   int n = 0;
   TL_CUDA(cudaGetDeviceCount(&n));
   if (device < 0 || device >= n) return fail(TL_ERR_CUDA, "device %d not present (%d devices)", device, n);
@@ -738,7 +751,8 @@ tl_status init_common(tl_comm* c, int world, int device, int64_t max_M, int64_t 
   c->sm_count = prop.multiProcessorCount;
   c->max_M = (max_M + world - 1) / world * world;
   c->max_H = (max_H + 7) / 8 * 8;
-  c->lay = WsLayout::make(world, c->max_M, c->max_H);
+  c->max_topk = max_topk;
+  c->lay = WsLayout::make(world, c->max_M, c->max_H, max_topk);
   apply_env(c->opt);
   return TL_OK;
 }
@@ -767,11 +781,16 @@ size_t tl_handle_size(void) { return sizeof(Handle); }
 
 tl_status tl_comm_create(int rank, int world, int device, int64_t max_M, int64_t max_H, void* my_handle,
                          tl_comm_t* out) {
+  return tl_comm_create_ex(rank, world, device, max_M, max_H, 1, my_handle, out);
+}
+
+tl_status tl_comm_create_ex(int rank, int world, int device, int64_t max_M, int64_t max_H, int max_topk,
+                            void* my_handle, tl_comm_t* out) {
   if (!out || !my_handle) return fail(TL_ERR_INVALID, "null out/my_handle");
   *out = nullptr;
   if (rank < 0 || rank >= world) return fail(TL_ERR_INVALID, "rank %d outside world %d", rank, world);
   tl_comm* c = new tl_comm;
-  tl_status st = init_common(c, world, device, max_M, max_H);
+  tl_status st = init_common(c, world, device, max_M, max_H, max_topk);
   if (st == TL_OK) {
     c->rank = rank;
     c->n_local = 1;
@@ -786,6 +805,7 @@ tl_status tl_comm_create(int rank, int world, int device, int64_t max_M, int64_t
     h.world = world;
     h.max_M = c->max_M;
     h.max_H = c->max_H;
+    h.max_topk = c->max_topk;
     h.ws_bytes = c->lay.bytes;
     if (world > 1) {
       cudaError_t e = cudaIpcGetMemHandle(&h.ipc, c->ws[rank]);
@@ -810,7 +830,7 @@ tl_status tl_comm_connect(tl_comm_t c, const void* all_handles) {
   for (int r = 0; r < c->world; ++r) {
     const Handle& h = hs[r];
     if (h.magic != kMagic || h.rank != r || h.world != c->world || h.max_M != c->max_M || h.max_H != c->max_H ||
-        h.ws_bytes != c->lay.bytes)
+        h.max_topk != c->max_topk || h.ws_bytes != c->lay.bytes)
       return fail(TL_ERR_INVALID, "handle %d does not match this comm (magic/rank/world/capacity)", r);
   }
   TL_CUDA(cudaSetDevice(c->device));
@@ -827,10 +847,15 @@ tl_status tl_comm_connect(tl_comm_t c, const void* all_handles) {
 }
 
 tl_status tl_comm_create_loopback(int world, int device, int64_t max_M, int64_t max_H, tl_comm_t* out) {
+  return tl_comm_create_loopback_ex(world, device, max_M, max_H, 1, out);
+}
+
+tl_status tl_comm_create_loopback_ex(int world, int device, int64_t max_M, int64_t max_H, int max_topk,
+                                     tl_comm_t* out) {
   if (!out) return fail(TL_ERR_INVALID, "null out");
   *out = nullptr;
   tl_comm* c = new tl_comm;
-  tl_status st = init_common(c, world, device, max_M, max_H);
+  tl_status st = init_common(c, world, device, max_M, max_H, max_topk);
   if (st == TL_OK) {
     c->loopback = true;
     c->rank = -1;
@@ -964,6 +989,137 @@ tl_status tl_mlp_forward_loopback(tl_comm_t c, const void* const* X, const void*
   if (!c || !c->loopback) return fail(TL_ERR_STATE, "not a loopback comm");
   if (!X || !W1 || !W2 || !out) return fail(TL_ERR_INVALID, "null pointer array");
   return mlp_impl(c, X, W1, W2, out, Z, M, H, I_l, act, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+namespace {
+// ---------------------------------------------------------------- MoE second half
+// GroupGEMM + Scatter + TopK reduce + ReduceScatter: the grouped GEMM's epilogue
+// scatters each weighted row straight into its owner's staging slot [src rank][token][k]; the last
+// CTA of every rank releases that rank's slot flag on every owner; an owner kernel then sums over
+// (src rank, k) in fp32 and rounds once.
+tl_status moe_gemm_rs_impl(tl_comm* c, const void* const* Zg, const int32_t* const* rows, const int32_t* const* offs,
+                           const float* const* topk_w, const void* const* W2, void* const* out, int64_t M, int64_t H,
+                           int64_t I_l, int E, int topk, cudaStream_t stream) {
+  tl_status st = check_comm(c);
+  if (st != TL_OK) return st;
+  const int W = c->world;
+  if (M < 1 || H < 8 || I_l < 8 || H % 8 || I_l % 8 || M % W)
+    return fail(TL_ERR_INVALID, "bad MoE shapes (M=%lld H=%lld I_l=%lld)", (long long)M, (long long)H, (long long)I_l);
+  if (E < 1 || E > 1024 || topk < 1 || topk > E) return fail(TL_ERR_INVALID, "MoE needs 1 <= topk <= E <= 1024");
+  if (topk > c->max_topk)
+    return fail(TL_ERR_UNSUPPORTED, "topk=%d exceeds the comm's max_topk=%d (tl_comm_create_ex)", topk, c->max_topk);
+  if (M > c->max_M || H > c->max_H) return fail(TL_ERR_INVALID, "M/H exceed comm capacity");
+  for (int i = 0; i < c->n_local; ++i)
+    if (!Zg[i] || !rows[i] || !offs[i] || !topk_w[i] || !W2[i] || !out[i] || !aligned16(Zg[i]) || !aligned16(W2[i]) ||
+        !aligned16(out[i]))
+      return fail(TL_ERR_INVALID, "null or misaligned pointer (rank slot %d)", i);
+  TL_CUDA(cudaSetDevice(c->device));
+  const int pair = pair_of(c);
+  const int BM = 128 * pair;
+  const int64_t R_cap = moe_capacity(M, topk, E, BM);
+  const int64_t M_r = M / W;
+  const uint32_t epoch = ++c->rs_epoch;
+  const int bank = epoch & 1;
+  Params* pp = new Params;
+  Params& p = *pp;
+  fill_common(c, p);
+  const int nsub = (pair == 2 && c->opt.n_sub != 1 && (c->opt.n_sub == 2 || H >= 512)) ? 2 : 1;
+  p.M = (int)R_cap;
+  p.N_out = (int)H;
+  p.K = (int)I_l;
+  p.M_r = (int)M_r;
+  p.epoch = epoch;
+  p.n_blocks = (int)((H + 256 * nsub - 1) / (256 * nsub));
+  p.k_blocks = (int)((I_l + kBK - 1) / kBK);
+  p.n_full = 1 << 30;
+  p.topk = topk;
+  p.tm_rows = p.tiles_per_rank = p.tiles_per_channel = 1;
+  p.moe_done_base = c->moe_done;
+  for (int o = 0; o < W; ++o) {
+    p.staging[o] = reinterpret_cast<const uint16_t*>(c->ws[o] + c->lay.stage[bank]);
+    p.moe_flags[o] = reinterpret_cast<uint32_t*>(c->ws[o] + c->lay.moe_sync);
+  }
+  const int max_tiles = (int)(R_cap / BM);
+  const size_t need = (size_t)(4 + 3 * max_tiles + max_tiles + 4) * sizeof(int);
+  for (int i = 0; st == TL_OK && i < c->n_local; ++i) {
+    RankArgs& ra = p.rk[i];
+    const int r = local_rank_id(c, i);
+    ra.rank = r;
+    if (c->moe_bytes[i] < need) {
+      if (c->moe_buf[i]) cudaFree(c->moe_buf[i]);
+      c->moe_buf[i] = nullptr;
+      c->moe_bytes[i] = 0;
+      cudaError_t e = cudaMalloc(&c->moe_buf[i], need);
+      if (e != cudaSuccess) { st = fail(TL_ERR_CUDA, "MoE table alloc: %s", cudaGetErrorString(e)); break; }
+      c->moe_bytes[i] = need;
+    }
+    int* tab = c->moe_buf[i];
+    int* sched = tab + 4 + 3 * max_tiles;
+    tl_moe_tiles_kernel<<<8, 256, 0, stream>>>(offs[i], E, BM, tab, sched);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { st = fail(TL_ERR_CUDA, "MoE tile table: %s", cudaGetErrorString(e)); break; }
+    ra.moe_rows = rows[i];
+    ra.moe_tab = tab;
+    ra.moe_sched = sched;
+    ra.moe_w = topk_w[i];
+    ra.moe_done = reinterpret_cast<unsigned*>(c->ws[r] + c->lay.moe_sync + 4096);
+    if ((st = cached_tmap(c, &ra.tm_a, Zg[i], R_cap, I_l, 128, 64)) != TL_OK) break;
+    const uint64_t kb = (uint64_t)I_l * 2;
+    const uint64_t dims[3] = {(uint64_t)I_l, (uint64_t)H, (uint64_t)E};
+    const uint64_t str[2] = {kb, kb * H};
+    const uint32_t box[3] = {64, (uint32_t)(pair == 2 ? 128 : 256), 1};
+    if ((st = make_tmap_nd(&ra.tm_b0, W2[i], 3, dims, str, box)) != TL_OK) break;
+  }
+  if (st == TL_OK) st = launch_moe(c, p, EPI_MOE_SCATTER, false, nsub, stream);
+  if (st == TL_OK) {
+    c->moe_done += (unsigned)p.ctas_per_rank;
+    MoeReduceArgs a;
+    memset(&a, 0, sizeof(a));
+    for (int i = 0; i < c->n_local; ++i) {
+      const int r = local_rank_id(c, i);
+      a.staging[i] = reinterpret_cast<const uint16_t*>(c->ws[r] + c->lay.stage[bank]);
+      a.flags[i] = reinterpret_cast<const uint32_t*>(c->ws[r] + c->lay.moe_sync);
+      a.out[i] = reinterpret_cast<uint16_t*>(out[i]);
+      a.rank[i] = r;
+    }
+    a.world = W;
+    a.M_r = (int)M_r;
+    a.topk = topk;
+    a.H = (int)H;
+    a.epoch = epoch;
+    a.timeout_ns = p.timeout_ns;
+    a.diag = p.diag;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((M_r * (H / 8) + 255) / 256, c->sm_count / c->n_local));
+    tl_moe_reduce_kernel<<<dim3(blocks, c->n_local), 256, 0, stream>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "MoE reduce: %s", cudaGetErrorString(e));
+  }
+  delete pp;
+  return st;
+}
+}  // namespace
+
+extern "C" {
+
+tl_status tl_moe_gemm_rs(tl_comm_t c, const void* Zg, const int32_t* row_ids, const int32_t* expert_offsets,
+                         const float* topk_weights, const void* W2, void* out_shard, int64_t M, int64_t H,
+                         int64_t I_local, int E, int topk, void* stream) {
+  if (c && c->loopback) return fail(TL_ERR_STATE, "loopback comm: use tl_moe_gemm_rs_loopback");
+  return moe_gemm_rs_impl(c, &Zg, &row_ids, &expert_offsets, &topk_weights, &W2, &out_shard, M, H, I_local, E, topk,
+                          (cudaStream_t)stream);
+}
+
+tl_status tl_moe_gemm_rs_loopback(tl_comm_t c, const void* const* Zg, const int32_t* const* row_ids,
+                                  const int32_t* const* expert_offsets, const float* const* topk_weights,
+                                  const void* const* W2, void* const* out_shard, int64_t M, int64_t H,
+                                  int64_t I_local, int E, int topk, void* stream) {
+  if (!c || !c->loopback) return fail(TL_ERR_STATE, "not a loopback comm");
+  if (!Zg || !row_ids || !expert_offsets || !topk_weights || !W2 || !out_shard)
+    return fail(TL_ERR_INVALID, "null pointer array");
+  return moe_gemm_rs_impl(c, Zg, row_ids, expert_offsets, topk_weights, W2, out_shard, M, H, I_local, E, topk,
+                          (cudaStream_t)stream);
 }
 
 int64_t tl_moe_capacity(tl_comm_t c, int64_t M, int topk, int E) {

@@ -191,7 +191,7 @@ __device__ __forceinline__ void epi_load(uint32_t tacc, int pc, float* r) {
   }
 }
 
-template <int kPair, int kStages, int kEpi, bool kAG, int kNSub, bool kMoE = false>
+template <int kPair, int kStages, int kEpi, bool kAG, int kNSub, int kMoE = MOE_NONE>
 __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_constant__ Params p) {
   using L = Layout<kPair, kStages, kAG, kNSub>;
   constexpr int kAccBufs = 2 / kNSub;          // TMEM accumulator buffers (512 columns in total)
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     }
   };
 
-  if (kMoE && (warp == 0 || warp == 2 || (!kAG && warp == 3))) {
+  if (kMoE == MOE_GATHER && (warp == 0 || warp == 2 || (!kAG && warp == 3))) {
     if (lane == 0) moe_produce(warp == 0, warp == 0 ? 0 : warp == 2 ? kGPer : 2 * kGPer);
   } else if (warp == 0) {
     // ============================== TMA producer ==============================
@@ -313,9 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       int stage = 0;
       uint32_t phase = 0;
       for (int item = pair; item < total; item += n_pairs) {
-        int t, sub_lo, sub_n, mb, nb;
+        int t, sub_lo, sub_n, mb, nb, expert = 0;
         item_coords<kNSub>(p, item, t, sub_lo, sub_n);
-        tile_coords(p, rank, ra.m_rot, t, mb, nb);
+        if constexpr (kMoE == MOE_SCATTER) moe_coords(p, ra, item, mb, nb, expert);
+        else tile_coords(p, rank, ra.m_rot, t, mb, nb);
         const int row0 = mb * BM + cta_in_pair * 128;
         if constexpr (kAG) {
           if (p.debug_mode != 1 && row0 < p.M) ag_wait_rows(p, rank, row0, min(row0 + 128, p.M));
@@ -328,7 +329,16 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
             uint8_t* sa = smem + L::off_a + stage * kAStage;
             uint8_t* sb = smem + L::off_b + stage * L::kBStage;
             const int kc = kb * kBK;
-            if constexpr (kPair == 2) {
+            if constexpr (kMoE == MOE_SCATTER) {   // grouped rows are contiguous; B = the tile's expert
+              if constexpr (kPair == 2) ptx::tma_load_2d_pair(&ra.tm_a, &full[stage], sa, kc, row0);
+              else ptx::tma_load_2d(&ra.tm_a, &full[stage], sa, kc, row0);
+#pragma unroll
+              for (int q = 0; q < NS; ++q) {
+                const int sub = s_lo + q;
+                ptx::tma_load_3d<kPair>(&ra.tm_b0, &full[stage], sb + sub * L::kBBox, kc,
+                                        nb * kAccCols + sub * kUmmaN + (kPair == 2 ? cta_in_pair * 128 : 0), expert);
+              }
+            } else if constexpr (kPair == 2) {
               ptx::tma_load_2d_pair(&ra.tm_a, &full[stage], sa, kc, row0);
 #pragma unroll
               for (int q = 0; q < NS; ++q) {
@@ -518,6 +528,18 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
           out_row = lrow0 + ew * 32;
         }
       }
+      // MoE scatter: this thread's grouped row -> (token, slot), router weight, owner staging row
+      uint16_t* moe_dst = nullptr;
+      float moe_wt = 0.f;
+      if constexpr (kEpi == EPI_MOE_SCATTER) {
+        const int rid = ra.moe_rows[row0 + ew * 32 + (int)lane];
+        if (rid >= 0) {
+          const int tok = rid / p.topk, kk = rid - tok * p.topk, o = tok / p.M_r;
+          moe_wt = ra.moe_w[rid];
+          moe_dst = const_cast<uint16_t*>(p.staging[o]) +
+                    (((size_t)rank * p.M_r + (tok - o * p.M_r)) * p.topk + kk) * (size_t)p.N_out;
+        }
+      }
       // piece -> 16 packed bf16x2 words (activation / slot reduction in fp32)
       auto compute = [&](float* r, int pc, uint32_t* out16) {
         if constexpr (kGated) {
@@ -536,6 +558,10 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
                 if (add_mask & (1u << s2)) add_slot32(r, stg + ((size_t)s2 * p.M_r + myrow) * p.N_out, col, p.N_out);
             }
           }
+          if constexpr (kEpi == EPI_MOE_SCATTER) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] *= moe_wt;   // top-k weight, applied before the bf16 transport
+          }
 #pragma unroll
           for (int i = 0; i < 16; ++i) out16[i] = ptx::pack_bf16x2(r[2 * i], r[2 * i + 1]);
         }
@@ -553,7 +579,19 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         if (pc + 2 == pc_end) release_tmem();
         else epi_load<kGated>(tacc, pc + 2, ra_);
         compute(rb_, pc + 1, pk + 16);
-        store_chunk(pk, bufs, sbuf, tm_out, out_col0 + pc * 32, out_row, lane);
+        if constexpr (kEpi == EPI_MOE_SCATTER) {
+          // tile_push_data p2p of one weighted row segment straight to the owner's staging slot
+          const int col = out_col0 + pc * 32;
+          if (moe_dst) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (col + 8 * j < p.N_out)
+                *reinterpret_cast<uint4*>(moe_dst + col + 8 * j) =
+                    make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
+        } else {
+          store_chunk(pk, bufs, sbuf, tm_out, out_col0 + pc * 32, out_row, lane);
+        }
         if (pc + 2 < pc_end) ptx::tmem_ld_wait_fence<kPW>(ra_);
       }
       if constexpr (kEpi == EPI_RS) {
@@ -569,6 +607,20 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     }
     if (lane == 0) ptx::bulk_wait<0>();
     __syncwarp();
+    if constexpr (kEpi == EPI_MOE_SCATTER) {
+      // every CTA of this rank counts itself done; the last one releases this rank's slot flag on
+      // every owner (peer_tile_notify at whole-operator granularity: the scatter targets are data
+      // dependent, so completion is per source rank)
+      __threadfence_system();
+      ptx::named_bar_sync(1, 128);
+      if (ew == 0 && lane == 0) {
+        const unsigned old = atomicAdd(ra.moe_done, 1u);
+        if (old == p.moe_done_base + (unsigned)p.ctas_per_rank - 1u) {
+          __threadfence_system();
+          for (int o = 0; o < p.world; ++o) ptx::st_release_sys(p.moe_flags[o] + rank, p.epoch);
+        }
+      }
+    }
   }
 
   ptx::tc_fence_before();
@@ -680,6 +732,61 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     int o = bcnt[tid];
     for (int t = 0; t < n_tiles; ++t)
       if (keys[t] == tid) sched[o++] = t;
+  }
+}
+
+// MoE owner reduction (TopK reduce + the reduce of ReduceScatter): once every source rank's slot
+// flag carries this epoch, out[t] = sum_s sum_k staging[s][t][k] in fp32 (ascending s, then k),
+// rounded once.  Grid: (row blocks, local ranks); one thread per 8 columns.
+struct MoeReduceArgs {
+  const uint16_t* staging[kMaxWorld];
+  const uint32_t* flags[kMaxWorld];
+  uint16_t* out[kMaxWorld];
+  int rank[kMaxWorld];
+  int world, M_r, topk, H;
+  uint32_t epoch;
+  uint64_t timeout_ns;
+  Diag* diag;
+};
+__global__ void __launch_bounds__(256) tl_moe_reduce_kernel(const __grid_constant__ MoeReduceArgs a) {
+  const int lr = blockIdx.y;
+  const int rank = a.rank[lr];
+  if (threadIdx.x < a.world)
+    flag_wait(a.flags[lr] + threadIdx.x, a.epoch, a.timeout_ns, a.diag, rank, 3, threadIdx.x, 0);
+  __syncthreads();
+  const int cpr = a.H / 8;                       // 16-byte chunks per row
+  const long long n = (long long)a.M_r * cpr;
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const int t = (int)(i / cpr), c = (int)(i % cpr) * 8;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int s = 0; s < a.world; ++s)
+      for (int k = 0; k < a.topk; ++k) {
+        const uint4 q = ptx::ld_global_v4(a.staging[lr] + (((size_t)s * a.M_r + t) * a.topk + k) * a.H + c);
+        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          acc[2 * e] += __uint_as_float(w4[e] << 16);
+          acc[2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+        }
+      }
+    *reinterpret_cast<uint4*>(a.out[lr] + (size_t)t * a.H + c) =
+        make_uint4(ptx::pack_bf16x2(acc[0], acc[1]), ptx::pack_bf16x2(acc[2], acc[3]),
+                   ptx::pack_bf16x2(acc[4], acc[5]), ptx::pack_bf16x2(acc[6], acc[7]));
+  }
+}
+
+// Tile table of a grouped layout from its padded group offsets (second MoE half): tab[0] = tiles,
+// tab[4 + 3 t] = expert of tile t; schedule = identity.
+__global__ void tl_moe_tiles_kernel(const int* offs, int E, int BM, int* tab, int* sched) {
+  const int n = offs[E] / BM;
+  if (threadIdx.x == 0 && blockIdx.x == 0) tab[0] = n;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    int e = 0;
+    while (offs[e + 1] <= t * BM) ++e;
+    tab[4 + 3 * t] = e;
+    tab[5 + 3 * t] = 0;
+    tab[6 + 3 * t] = 0;
+    sched[t] = t;
   }
 }
 

@@ -13,7 +13,10 @@ constexpr int kMaxWorld = 8;
 constexpr int kAgFlagStride = 4096;   // producer tiles per source rank (flags per source)
 constexpr int kRsFlagStride = 16384;  // CTA tiles per owner block (flags per slot)
 
-enum Epi : int { EPI_STORE = 0, EPI_SILU_MUL = 1, EPI_GELU_MUL = 2, EPI_RS = 3 };
+enum Epi : int { EPI_STORE = 0, EPI_SILU_MUL = 1, EPI_GELU_MUL = 2, EPI_RS = 3, EPI_MOE_SCATTER = 4 };
+// MoE kernel flavours: 1 = AG + gather + GroupGEMM (rows gathered by token id), 2 = grouped GEMM
+// whose epilogue scatters weighted rows to the owners' staging slots (GroupGEMM + Scatter + TopK + RS)
+enum MoeKind : int { MOE_NONE = 0, MOE_GATHER = 1, MOE_SCATTER = 2 };
 enum Order : int { ORDER_IDENTITY = 0, ORDER_AG_INTERLEAVE = 1, ORDER_ROTATE = 2 };
 enum RsMode : int { RS_NONE = 0, RS_ONESHOT = 1, RS_RING = 2 };
 
@@ -31,6 +34,8 @@ struct alignas(64) RankArgs {
   const int* moe_rows;
   const int* moe_tab;
   const int* moe_sched;
+  const float* moe_w;         // MoE scatter: router weights [M, topk] (index = row id)
+  unsigned int* moe_done;     // MoE scatter: this rank's CTA completion counter
 };
 
 struct alignas(64) Params {
@@ -57,6 +62,8 @@ struct alignas(64) Params {
   // A read from whatever X_full holds), 2 = communication only (only the AG copy role runs)
   int debug_mode;
   int topk;           // MoE: routed slots per token
+  unsigned int moe_done_base;       // MoE scatter: counter value before this call
+  uint32_t* moe_flags[kMaxWorld];   // MoE scatter: [W slots] completion flags of rank o
 };
 
 }  // namespace tl

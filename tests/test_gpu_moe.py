@@ -95,3 +95,70 @@ def test_moe_paper_shape_moe4_w8(tl):
     (N_out = I/8 = 256 per expert shard), loopback on one GPU."""
     res = _run(tl, 8, M=8192, H=4096, E=8, topk=2, N_out=256, act=TI.ACT_SILU_MUL)
     _check(*res)
+
+
+# ----------------------------------------------------------------------------- MoE second half + full layer
+def _moe_layer(tl, W, M, H, I, E, topk, act=TI.ACT_SILU_MUL, skew=0.0, calls=1, pair=2, nsub=0, seed=0):
+    il = I // W
+    X = TI._randn((M, H), seed, 0)
+    Xs = TI.shard_rows(X, W)
+    W1s = TI.moe_weights(E, 2 * il, H, W, seed=seed + 1)
+    W2s = TI.moe_down_weights(E, H, il, W, seed=seed + 3)
+    ids = TI.moe_routing(M, E, topk, seed=seed + 2, skew=skew)
+    wts = TI.moe_topk_weights(M, topk, seed=seed + 4)
+    comm = (tl.Comm.loopback(W, 0, max_M=M, max_H=H, max_topk=topk) if W > 1
+            else tl.Comm.single(0, max_M=M, max_H=H, max_topk=topk))
+    comm.set_option("cta_pair", pair)
+    comm.set_option("n_sub", nsub)
+    R = tl.moe_capacity(comm, M, topk, E)
+    Zg = [torch.empty(R, il, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    rows = [torch.empty(R, device="cuda", dtype=torch.int32) for _ in range(W)]
+    offs = [torch.empty(E + 1, device="cuda", dtype=torch.int32) for _ in range(W)]
+    outs = [torch.empty(M // W, H, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    xd, idd, w1d, w2d, wtd = ([x.cuda() for x in Xs], [ids.cuda() for _ in range(W)], [w.cuda() for w in W1s],
+                              [w.cuda() for w in W2s], [wts.cuda() for _ in range(W)])
+    results = []
+    for _ in range(calls):
+        if W > 1:
+            tl.moe_ag_gemm_lb(comm, xd, idd, w1d, Zg, rows, offs, act=act)
+            tl.moe_gemm_rs_lb(comm, Zg, rows, offs, wtd, w2d, outs)
+            st, diag = comm.check()
+            assert st == 0, diag
+        else:
+            tl.moe_ag_gemm(comm, xd[0], idd[0], w1d[0], Zg[0], rows[0], offs[0], act=act)
+            tl.moe_gemm_rs(comm, Zg[0], rows[0], offs[0], wtd[0], w2d[0], outs[0])
+            st, diag = comm.check()
+            assert st == 0, diag
+        results.append([o.clone() for o in outs])
+    f = lambda L: [TI.to_f64(t) for t in L]
+    ref = O.moe_forward(f(Xs), ids.numpy(), wts.double().numpy(), f(W1s), f(W2s), act)
+    return results, ref
+
+
+@pytest.mark.parametrize("W", [1, 2, 4, 8])
+@pytest.mark.parametrize("topk", [2, 5])
+def test_moe_layer_parity(tl, W, topk):
+    """Full TP MoE FFN: AG + Gather + GroupGEMM + SiLU*up, then GroupGEMM + Scatter + TopK + RS."""
+    results, ref = _moe_layer(tl, W, M=256 * W if W > 1 else 512, H=256, I=256 * W, E=8, topk=topk)
+    got = np.concatenate([o.float().cpu().double().numpy() for o in results[0]], 0)
+    assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
+
+
+@pytest.mark.parametrize("pair,nsub", [(1, 1), (2, 1), (2, 2)])
+def test_moe_layer_options_and_epochs(tl, pair, nsub):
+    """Tile shapes / CTA pairing never change the result beyond rounding; repeated calls (banks and
+    epochs cycling, completion counters accumulating) are bitwise identical."""
+    results, ref = _moe_layer(tl, 4, M=1024, H=512, I=1024, E=16, topk=3, skew=1.0, calls=4, pair=pair, nsub=nsub)
+    got = np.concatenate([o.float().cpu().double().numpy() for o in results[0]], 0)
+    assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
+    for later in results[1:]:
+        for a, b in zip(later, results[0]):
+            assert torch.equal(a, b)
+
+
+def test_moe_layer_single_expert_matches_dense_mlp_kernels(tl):
+    """E = 1, top-1, weight 1: the MoE path must agree with the dense MLP path on the GPU."""
+    W, M, H, I = 2, 512, 256, 512
+    results, ref = _moe_layer(tl, W, M, H, I, E=1, topk=1)
+    got = np.concatenate([o.float().cpu().double().numpy() for o in results[0]], 0)
+    assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
