@@ -70,7 +70,30 @@ def run(name, S, H, I, E, topk, W=1):
         got = Y[g].float().cpu().double().numpy()
         err_num += float(((got - ref) ** 2).sum())
         err_den += float((ref ** 2).sum())
+    # second half: GroupGEMM + Scatter + TopK reduce (+RS, W = 1 here) on the grouped output
+    c2 = tl.Comm.single(0, max_M=S, max_H=H, max_topk=topk)
+    W2t = TI.moe_down_weights(E, H, il, 1, seed=3)[0].cuda()
+    wts = TI.moe_topk_weights(S, topk, seed=4).cuda()
+    out = torch.empty(S, H, device="cuda", dtype=torch.bfloat16)
+    ms2 = timeit(lambda: tl.moe_gemm_rs(c2, Y, rows, offs, wts, W2t, out))
+    fl2 = 2.0 * S * topk * il * H
+
+    def base2():
+        z = Y[:S * topk]                                   # same amount of grouped work
+        outs, o = [], 0
+        for e in range(E):
+            n = counts[e]
+            outs.append(z[o:o + n] @ W2t[e].T)
+            o += n
+        p = torch.cat(outs) * wts.flatten()[order].unsqueeze(1).to(torch.bfloat16)
+        res = torch.zeros(S, H, device="cuda", dtype=torch.float32)
+        res.index_add_(0, tok, p.float())
+        return res
+    bms2 = timeit(base2)
     r = {"name": name, "S": S, "H": H, "I": I, "E": E, "topk": topk, "W": W, "ms": round(ms, 4),
+         "second_half_ms": round(ms2, 4), "second_half_tflops": round(fl2 / ms2 / 1e9, 1),
+         "torch_second_half_ms": round(bms2, 4), "layer_ms": round(ms + ms2, 4),
+         "layer_speedup_vs_torch": round((bms + bms2) / (ms + ms2), 3),
          "tflops": round(fl / ms / 1e9, 1), "torch_gather_cublas_ms": round(bms, 4),
          "speedup": round(bms / ms, 3), "padding_rows": int(R - S * topk),
          "parity_rel_fro_sampled": (err_num / err_den) ** 0.5}
