@@ -559,7 +559,12 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
     const int max_tiles = (int)(moe->R_cap / BM);
     p.topk = moe->topk;
     const size_t need = (size_t)(4 + 3 * max_tiles + max_tiles + 4) * sizeof(int);
-    const size_t smem = (size_t)(2 * moe->E + 64 * moe->E + moe->E + 1 + max_tiles + kMoeThreads) * sizeof(int);
+    const size_t smem = (size_t)(32 * moe->E + 2 * moe->E + 1 + max_tiles + kMoeThreads) * sizeof(int);
+    // schedule key: expected-arrival bucket (W > 1) coarsened to <= 4 buckets, then expert
+    int key_shift = 0;
+    if (W == 1) key_shift = 30;
+    else
+      while ((((M_r + sm.Tm - 1) / sm.Tm) >> key_shift) > 4) ++key_shift;
     if (smem > 227 * 1024) st = fail(TL_ERR_UNSUPPORTED, "MoE table build needs %zu B of smem", smem);
     for (int i = 0; st == TL_OK && i < c->n_local; ++i) {
       if (c->moe_bytes[i] < need) {
@@ -575,8 +580,8 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
       int* err = sched + max_tiles;
       cudaFuncSetAttribute(tl_moe_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       tl_moe_tables_kernel<<<1, kMoeThreads, smem, stream>>>(moe->topk_ids[i], (int)(M * moe->topk), moe->topk,
-                                                             moe->E, BM, (int)M_r, sm.Tm, moe->rows[i], moe->offs[i],
-                                                             tab, sched, max_tiles, err);
+                                                             moe->E, BM, (int)M_r, sm.Tm, key_shift, moe->rows[i],
+                                                             moe->offs[i], tab, sched, max_tiles, err);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) { st = fail(TL_ERR_CUDA, "MoE table kernel: %s", cudaGetErrorString(e)); break; }
       p.rk[i].moe_rows = moe->rows[i];
@@ -1091,7 +1096,8 @@ tl_status moe_gemm_rs_impl(tl_comm* c, const void* const* Zg, const int32_t* con
     a.epoch = epoch;
     a.timeout_ns = p.timeout_ns;
     a.diag = p.diag;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((M_r * (H / 8) + 255) / 256, c->sm_count / c->n_local));
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((M_r * (H / 8) + 255) / 256,
+                                                                  8ll * c->sm_count / c->n_local));
     tl_moe_reduce_kernel<<<dim3(blocks, c->n_local), 256, 0, stream>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "MoE reduce: %s", cudaGetErrorString(e));

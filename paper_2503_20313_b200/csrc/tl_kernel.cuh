@@ -104,9 +104,16 @@ __device__ __forceinline__ void item_coords(const Params& p, int item, int& t, i
 // arrival), n-blocks innermost so a gathered A block is reused from L2.
 __device__ __forceinline__ void moe_coords(const Params& p, const RankArgs& ra, int item, int& mt, int& nb,
                                            int& expert) {
-  const int j = item / p.n_blocks;
-  nb = item - j * p.n_blocks;
-  mt = ra.moe_sched[j];
+  // grouped rasterisation over the schedule: G consecutive scheduled tiles (same arrival bucket,
+  // sorted by expert) x all n-blocks, tiles fastest, so concurrent tiles share the expert's B block
+  const int G = p.raster_group, n_tiles = ra.moe_tab[0];
+  const int per_group = G * p.n_blocks;
+  const int group = item / per_group;
+  const int first = group * G;
+  const int rows = min(G, n_tiles - first);
+  const int local = item - group * per_group;
+  nb = local / rows;
+  mt = ra.moe_sched[first + local % rows];
   expert = ra.moe_tab[4 + 3 * mt];
 }
 
@@ -580,15 +587,32 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         else epi_load<kGated>(tacc, pc + 2, ra_);
         compute(rb_, pc + 1, pk + 16);
         if constexpr (kEpi == EPI_MOE_SCATTER) {
-          // tile_push_data p2p of one weighted row segment straight to the owner's staging slot
+          // tile_push_data p2p of weighted row segments to the owners' staging slots.  The warp's 32
+          // rows x 64 columns are transposed through its smem buffer so that every store instruction
+          // writes 4 whole 128-byte row segments (coalesced) instead of 32 scattered 16-byte pieces.
           const int col = out_col0 + pc * 32;
-          if (moe_dst) {
+          const uint32_t buf = ptx::smem_u32(bufs + sbuf * 4096);
+          sbuf ^= 1;
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (col + 8 * j < p.N_out)
-                *reinterpret_cast<uint4*>(moe_dst + col + 8 * j) =
-                    make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          for (int j = 0; j < 8; ++j)
+            ptx::st_shared_v4(buf + lane * 128 + ((j ^ (lane & 7)) << 4), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2],
+                              pk[4 * j + 3]);
+          __syncwarp();
+          const unsigned long long mydst = reinterpret_cast<unsigned long long>(moe_dst);
+          const int c16 = lane & 7;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int q = i * 4 + (int)(lane >> 3);           // row of the warp slice written now
+            const unsigned long long d = __shfl_sync(0xffffffffu, mydst, q);
+            if (d != 0ull && col + c16 * 8 < p.N_out) {
+              uint4 v;
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                           : "r"(buf + q * 128 + ((c16 ^ (q & 7)) << 4)));
+              *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(d) + col + c16 * 8) = v;
+            }
           }
+          __syncwarp();
         } else {
           store_chunk(pk, bufs, sbuf, tm_out, out_col0 + pc * 32, out_row, lane);
         }
@@ -642,66 +666,74 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
 // Every rank builds identical tables from the identical routing: no communication.
 constexpr int kMoeThreads = 1024;
 __global__ void __launch_bounds__(kMoeThreads, 1)
-    tl_moe_tables_kernel(const int* __restrict__ ids, int n, int topk, int E, int BM, int M_r, int Tm, int* rows,
-                         int* offs, int* tab, int* sched, int max_tiles, int* err) {
+    tl_moe_tables_kernel(const int* __restrict__ ids, int n, int topk, int E, int BM, int M_r, int Tm,
+                         int key_shift, int* rows, int* offs, int* tab, int* sched, int max_tiles, int* err) {
   extern __shared__ int sh[];
-  int* cnt = sh;                 // [E]
-  int* base = cnt + E;           // [E]
-  int* wcnt = base + E;          // [32][E]
-  int* wpre = wcnt + 32 * E;     // [32][E]
-  int* soffs = wpre + 32 * E;    // [E + 1]
+  int* wcnt = sh;                // [32 warps][E] per-warp counts, then per-warp running positions
+  int* cnt = wcnt + 32 * E;      // [E]
+  int* soffs = cnt + E;          // [E + 1]
   int* keys = soffs + E + 1;     // [max_tiles]
   int* bcnt = keys + max_tiles;  // [kMoeThreads] bucket counts -> starts
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int e = tid; e < E; e += kMoeThreads) cnt[e] = 0;
+  // each warp owns one contiguous chunk of the routed entries (stable order = chunk order)
+  const int chunk = (n + 31) / 32, lo = warp * chunk, hi = min(lo + chunk, n);
+  for (int x = tid; x < 32 * E; x += kMoeThreads) wcnt[x] = 0;
   __syncthreads();
-  for (int i = tid; i < n; i += kMoeThreads) {
-    const int e = ids[i];
-    if (e < 0 || e >= E) atomicExch(err, 1);
-    else atomicAdd(&cnt[e], 1);
+  for (int i0 = lo; i0 < hi; i0 += 32) {       // pass 1: per-warp expert histogram (warp-private smem)
+    const int i = i0 + lane;
+    int e = i < hi ? ids[i] : -1;
+    if (e >= E || (i < hi && e < 0)) {
+      atomicExch(err, 1);
+      e = -1;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    if (e >= 0 && (peers & ((1u << lane) - 1u)) == 0) wcnt[warp * E + e] += __popc(peers);
+    __syncwarp();
   }
   __syncthreads();
+  // padded group offsets, then per-warp starting positions (exclusive scan over warps per expert)
   if (tid == 0) {
     int o = 0;
     for (int e = 0; e < E; ++e) {
+      int c = 0;
+      for (int w = 0; w < 32; ++w) c += wcnt[w * E + e];
+      cnt[e] = c;
       soffs[e] = o;
-      o += (cnt[e] + BM - 1) / BM * BM;
+      o += (c + BM - 1) / BM * BM;
     }
     soffs[E] = o;
     tab[0] = o / BM;
   }
   __syncthreads();
+  for (int e = tid; e < E; e += kMoeThreads) {
+    int run = soffs[e];
+    for (int w = 0; w < 32; ++w) {
+      const int c = wcnt[w * E + e];
+      wcnt[w * E + e] = run;
+      run += c;
+    }
+  }
   for (int e = tid; e <= E; e += kMoeThreads) offs[e] = soffs[e];
-  for (int e = tid; e < E; e += kMoeThreads) base[e] = soffs[e];
-  // stable counting sort: blocks of 1024 entries in order; rank inside a warp by __match_any,
-  // warp offsets by a per-expert scan over the 32 warps, expert bases carried across blocks
-  for (int b0 = 0; b0 < n; b0 += kMoeThreads) {
-    for (int x = tid; x < 32 * E; x += kMoeThreads) wcnt[x] = 0;
-    __syncthreads();
-    const int i = b0 + tid;
-    int e = i < n ? ids[i] : -1;
+  __syncthreads();
+  for (int i0 = lo; i0 < hi; i0 += 32) {       // pass 2: place entries, stable inside each warp chunk
+    const int i = i0 + lane;
+    int e = i < hi ? ids[i] : -1;
     if (e >= E) e = -1;
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     const int lrank = __popc(peers & ((1u << lane) - 1u));
-    if (e >= 0 && lrank == 0) wcnt[warp * E + e] = __popc(peers);
-    __syncthreads();
-    for (int x = tid; x < E; x += kMoeThreads) {
-      int run = base[x];
-      for (int w = 0; w < 32; ++w) {
-        wpre[w * E + x] = run;
-        run += wcnt[w * E + x];
-      }
-      base[x] = run;
-    }
-    __syncthreads();
-    if (e >= 0) rows[wpre[warp * E + e] + lrank] = i;
-    __syncthreads();
+    if (e >= 0) rows[wcnt[warp * E + e] + lrank] = i;
+    __syncwarp();
+    if (e >= 0 && lrank == 0) wcnt[warp * E + e] += __popc(peers);
+    __syncwarp();
   }
   for (int e = 0; e < E; ++e)
     for (int g = soffs[e] + cnt[e] + tid; g < soffs[e + 1]; g += kMoeThreads) rows[g] = -1;
   __syncthreads();
   const int n_tiles = soffs[E] / BM;
-  const int n_buckets = min((M_r + Tm - 1) / Tm, kMoeThreads);
+  // tile table + schedule key: (producer tile of the tile's last token) >> key_shift, then expert,
+  // so tiles of one expert that become ready together run together (their B blocks shared in L2)
+  const int n_keys = ((M_r + Tm - 1) / Tm + (1 << key_shift) - 1) >> key_shift;
+  const int n_buckets = min(n_keys * E, kMoeThreads);
   for (int x = tid; x < kMoeThreads; x += kMoeThreads) bcnt[x] = 0;
   __syncthreads();
   for (int t = tid; t < n_tiles; t += kMoeThreads) {
@@ -709,13 +741,12 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     int e = 0;
     while (soffs[e + 1] <= g0) ++e;
     const int last = min(g0 + BM, soffs[e] + cnt[e]) - 1;
-    const int lo = rows[g0] / topk, hi = rows[last] / topk;
+    const int tlo = rows[g0] / topk, thi = rows[last] / topk;
     tab[4 + 3 * t] = e;
-    tab[5 + 3 * t] = lo;
-    tab[6 + 3 * t] = hi;
-    // key: the producer tile (arrival slot) of the latest row this tile needs
-    const int key = (lo / M_r == hi / M_r) ? (hi % M_r) / Tm : (M_r - 1) / Tm;
-    keys[t] = min(key, n_buckets - 1);
+    tab[5 + 3 * t] = tlo;
+    tab[6 + 3 * t] = thi;
+    const int key = ((tlo / M_r == thi / M_r) ? (thi % M_r) / Tm : (M_r - 1) / Tm) >> key_shift;
+    keys[t] = min(key * E + e, n_buckets - 1);
     atomicAdd(&bcnt[keys[t]], 1);
   }
   __syncthreads();
@@ -756,19 +787,34 @@ __global__ void __launch_bounds__(256) tl_moe_reduce_kernel(const __grid_constan
   __syncthreads();
   const int cpr = a.H / 8;                       // 16-byte chunks per row
   const long long n = (long long)a.M_r * cpr;
+  const int terms = a.world * a.topk;
+  const size_t slot_stride = (size_t)a.M_r * a.topk * a.H;   // elements between source-rank slots
   for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
     const int t = (int)(i / cpr), c = (int)(i % cpr) * 8;
+    const uint16_t* base = a.staging[lr] + (size_t)t * a.topk * a.H + c;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int s = 0; s < a.world; ++s)
-      for (int k = 0; k < a.topk; ++k) {
-        const uint4 q = ptx::ld_global_v4(a.staging[lr] + (((size_t)s * a.M_r + t) * a.topk + k) * a.H + c);
-        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+    for (int j0 = 0; j0 < terms; j0 += 8) {      // 8 independent 16-byte loads in flight
+      uint4 q[8];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          acc[2 * e] += __uint_as_float(w4[e] << 16);
-          acc[2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u;
+        if (j < terms) {
+          const int s = j / a.topk, k = j - s * a.topk;   // ascending source rank, then slot
+          q[u] = ptx::ld_global_v4(base + s * slot_stride + (size_t)k * a.H);
         }
       }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (j0 + u < terms) {
+          const uint32_t w4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            acc[2 * e] += __uint_as_float(w4[e] << 16);
+            acc[2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+          }
+        }
+      }
+    }
     *reinterpret_cast<uint4*>(a.out[lr] + (size_t)t * a.H + c) =
         make_uint4(ptx::pack_bf16x2(acc[0], acc[1]), ptx::pack_bf16x2(acc[2], acc[3]),
                    ptx::pack_bf16x2(acc[4], acc[5]), ptx::pack_bf16x2(acc[6], acc[7]));
