@@ -505,6 +505,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
       if ((st = cached_tmap(c, &ra.tm_c, C[i], c_rows, N_out, 32, 64)) != TL_OK) break;
       continue;
     }
+    if ((st = cached_tmap(c, &ra.tm_a, a_src, M, K, 128, 64)) != TL_OK) break;
     if (act == TL_ACT_NONE) {
       if ((st = cached_tmap(c, &ra.tm_b0, B[i], N_out, K, pair == 2 ? 128 : 256, 64)) != TL_OK) break;
     } else {
