@@ -265,3 +265,30 @@ def moe_forward(X_shards, topk_ids, topk_weights, W1_list, W2_list, act: int):
     rows, Zs = moe_ag_group_gemm(X_shards, topk_ids, W1_list, act)
     M = sum(np.asarray(x).shape[0] for x in X_shards)
     return moe_group_gemm_rs(rows, Zs, W2_list, topk_weights, M)
+
+
+# ----------------------------------------------------------------------------
+# Sequence-parallel attention: AllGather KV + self-attention
+# ----------------------------------------------------------------------------
+def softmax_rows(S):
+    """Row softmax: exp(S - max) / sum(exp(S - max)) (the max shift is exact algebra)."""
+    S = np.asarray(S, dtype=np.float64)
+    E = np.exp(S - S.max(axis=1, keepdims=True))
+    return E / E.sum(axis=1, keepdims=True)
+
+
+def sp_attention(Q_shards, K_shards, V_shards, scale: float):
+    """"the context (key and value) is sharded across devices. Before computation, these context
+    shards are gathered to form a complete context for self-attention".  Shards are [S_r, heads, D];
+    K = AllGather(K_r), V = AllGather(V_r); O_r[:, h] = softmax(scale * Q_r[:, h] K[:, h]^T) V[:, h]
+    (non-causal).  Returns [O_r]."""
+    K = all_gather_rows(K_shards)
+    V = all_gather_rows(V_shards)
+    outs = []
+    for Q in Q_shards:
+        Q = np.asarray(Q, dtype=np.float64)
+        O = np.zeros_like(Q)
+        for h in range(Q.shape[1]):
+            O[:, h] = softmax_rows(scale * (Q[:, h] @ K[:, h].T)) @ V[:, h]
+        outs.append(O)
+    return outs

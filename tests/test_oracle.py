@@ -310,3 +310,39 @@ def test_moe_second_half_closed_form_and_brute_force():
                     if tt == t:
                         ref += w[t, k] * sum(Zg[r][j, i] * W2[r][e, h, i] for i in range(Il))
             assert abs(outs[t // (M // W)][t % (M // W), h] - ref) < 1e-12
+
+
+# --- sequence-parallel attention (NEXT-4): pins ------------------------------------
+def test_attention_closed_forms():
+    W, S, Hh, D = 2, 8, 2, 4
+    Qs, Ks, Vs = TI.attention_inputs(S, Hh, D, W, seed=1)
+    f = lambda L: [TI.to_f64(t) for t in L]
+    # equal keys -> uniform weights -> every output row is the mean of V (per head)
+    Kc = [np.ones_like(k) for k in f(Ks)]
+    outs = O.sp_attention(f(Qs), Kc, f(Vs), 0.5)
+    Vall = np.concatenate(f(Vs), 0)
+    for o in outs:
+        np.testing.assert_allclose(o, np.broadcast_to(Vall.mean(0), o.shape), rtol=1e-12, atol=1e-12)
+    # V = 0 -> O = 0; V = const -> O = const
+    assert all(np.all(o == 0) for o in O.sp_attention(f(Qs), f(Ks), [np.zeros_like(v) for v in f(Vs)], 0.3))
+    outs = O.sp_attention(f(Qs), f(Ks), [np.full_like(v, 2.5) for v in f(Vs)], 0.3)
+    assert all(np.allclose(o, 2.5, rtol=1e-14) for o in outs)
+
+
+def test_attention_kv_permutation_invariance_and_brute_force():
+    W, S, Hh, D = 2, 6, 1, 3
+    Qs, Ks, Vs = TI.attention_inputs(S, Hh, D, W, seed=2)
+    f = lambda L: [TI.to_f64(t) for t in L]
+    a = O.sp_attention(f(Qs), f(Ks), f(Vs), 0.7)
+    b = O.sp_attention(f(Qs), f(Ks)[::-1], f(Vs)[::-1], 0.7)       # gather order of the shards
+    for x, y in zip(a, b):
+        np.testing.assert_allclose(x, y, rtol=1e-13, atol=1e-14)
+    # pure-Python softmax(q.k) v for one row
+    K = [r for k in Ks for r in k.float().tolist()]
+    V = [r for v in Vs for r in v.float().tolist()]
+    q = Qs[1].float().tolist()[2][0]
+    sc = [0.7 * sum(qi * ki for qi, ki in zip(q, kr[0])) for kr in K]
+    mx = max(sc)
+    e = [math.exp(x - mx) for x in sc]
+    want = [sum(ei * vr[0][d] for ei, vr in zip(e, V)) / sum(e) for d in range(D)]
+    np.testing.assert_allclose(a[1][2, 0], want, rtol=1e-12)

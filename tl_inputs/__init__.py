@@ -188,3 +188,11 @@ def moe_topk_weights(M: int, topk: int, seed: int = 0):
 def moe_down_weights(E: int, H: int, I_l: int, W: int, seed: int = 0):
     """Per-rank expert down projections [E, H, I_l] bf16 ~ N(0, 1/(W * I_l))."""
     return [_randn((E, H, I_l), seed + 19 * r, _TID_W2, (W * I_l) ** -0.5) for r in range(W)]
+
+
+def attention_inputs(S: int, heads: int, D: int, W: int, seed: int = 0):
+    """Q, K, V ~ N(0, 1) [S, heads, D] bf16, row-sharded along the sequence over W ranks."""
+    Q = _randn((S, heads, D), seed, 10)
+    K = _randn((S, heads, D), seed, 11)
+    V = _randn((S, heads, D), seed, 12)
+    return shard_rows(Q, W), shard_rows(K, W), shard_rows(V, W)
