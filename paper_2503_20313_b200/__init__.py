@@ -15,7 +15,8 @@ ACT_NONE, ACT_SILU_MUL, ACT_GELU_TANH_MUL = 0, 1, 2
 ACTS = {"none": ACT_NONE, "silu_mul": ACT_SILU_MUL, "gelu_tanh_mul": ACT_GELU_TANH_MUL}
 
 __all__ = ["Comm", "TLError", "lib", "ACT_NONE", "ACT_SILU_MUL", "ACT_GELU_TANH_MUL", "static_map_device",
-           "moe_capacity", "moe_ag_gemm", "moe_ag_gemm_lb", "moe_gemm_rs", "moe_gemm_rs_lb"]
+           "moe_capacity", "moe_ag_gemm", "moe_ag_gemm_lb", "moe_gemm_rs", "moe_gemm_rs_lb", "sp_attention",
+           "sp_attention_lb"]
 
 
 def _ptr(t):
@@ -212,6 +213,28 @@ def moe_gemm_rs_lb(comm, Zgs, row_ids, offsets, topk_weights, W2s, outs, stream=
     check(lib().tl_moe_gemm_rs_loopback(comm._h, *[a[0] for a in arrs], M, H, I_l, E, topk, _stream(stream)),
           "tl_moe_gemm_rs_loopback")
     return outs
+
+
+def sp_attention(comm, Q_shard, K_shard, V_shard, O_shard, scale: float | None = None, stream=None):
+    """Sequence-parallel attention: AllGather(K, V) fused with flash attention (tl_sp_attention).
+    Q/K/V/O shards: contiguous bf16 CUDA tensors [S/world, heads, 128]."""
+    S_r, heads, D = Q_shard.shape
+    for n, t in (("Q", Q_shard), ("K", K_shard), ("V", V_shard), ("O", O_shard)):
+        _bf16(t, n)
+    scale = D ** -0.5 if scale is None else scale
+    check(lib().tl_sp_attention(comm._h, _ptr(Q_shard), _ptr(K_shard), _ptr(V_shard), _ptr(O_shard), S_r * comm.world,
+                                heads, D, scale, _stream(stream)), "tl_sp_attention")
+    return O_shard
+
+
+def sp_attention_lb(comm, Qs, Ks, Vs, Os, scale: float | None = None, stream=None):
+    """Loopback variant: per-rank lists of shards."""
+    S_r, heads, D = Qs[0].shape
+    scale = D ** -0.5 if scale is None else scale
+    arrs = [ptr_array([_ptr(t) for t in L]) for L in (Qs, Ks, Vs, Os)]
+    check(lib().tl_sp_attention_loopback(comm._h, *[a[0] for a in arrs], S_r * comm.world, heads, D, scale,
+                                         _stream(stream)), "tl_sp_attention_loopback")
+    return Os
 
 
 def static_map_device(M: int, world: int, tm_rows: int, channels_per_rank: int, n: int):

@@ -40,6 +40,8 @@ SIGNATURES = {
     "tl_comm_create_loopback_ex": (_int, [_int, _int, _i64, _i64, _int, C.POINTER(_vp)]),
     "tl_moe_gemm_rs": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp]),
     "tl_moe_gemm_rs_loopback": (_int, [_vp, _vpp, _vpp, _vpp, _vpp, _vpp, _vpp, _i64, _i64, _i64, _int, _int, _vp]),
+    "tl_sp_attention": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _int, _int, C.c_float, _vp]),
+    "tl_sp_attention_loopback": (_int, [_vp, _vpp, _vpp, _vpp, _vpp, _i64, _int, _int, C.c_float, _vp]),
     "tl_moe_ag_gemm": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _int, _vp]),
     "tl_moe_ag_gemm_loopback": (_int, [_vp, _vpp, _vpp, _vpp, _vpp, _vpp, _vpp, _i64, _i64, _i64, _int, _int, _int,
                                        _vp]),

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cctype>
+#include <cmath>
 #include <cstdarg>
 
 #include <cstdio>
@@ -17,6 +18,7 @@
 #include <tuple>
 
 #include "../../include/tl_api.h"
+#include "tl_attn.cuh"
 #include "tl_kernel.cuh"
 #include "tl_params.h"
 
@@ -1167,6 +1169,120 @@ tl_status tl_debug_static_map(int64_t M, int world, int64_t tm_rows, int channel
   cudaFree(d);
   if (e != cudaSuccess) return fail(TL_ERR_CUDA, "static map kernel: %s", cudaGetErrorString(e));
   return TL_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// ---------------------------------------------------------------- SP attention (NEXT-4)
+// AllGather of the K/V sequence shards fused with a tcgen05 flash-attention forward (P:54, P:474,
+// P:654-664).  The gathered K and V occupy the AG bank of the workspace: K at 0, V at S*heads*D*2.
+tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, const void* const* V, void* const* O,
+                    int64_t S, int heads, int D, float scale, cudaStream_t stream) {
+  tl_status st = check_comm(c);
+  if (st != TL_OK) return st;
+  const int W = c->world;
+  if (S < 0 || heads < 0) return fail(TL_ERR_INVALID, "negative dimension");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(TL_ERR_INVALID, "scale must be positive and finite");
+  if (S % W) return fail(TL_ERR_INVALID, "S=%lld not divisible by world=%d", (long long)S, W);
+  if (D != 128) return fail(TL_ERR_UNSUPPORTED, "head_dim must be 128 (got %d)", D);
+  const int64_t S_r = S / W;
+  if (S_r % 128) return fail(TL_ERR_UNSUPPORTED, "S/world must be a multiple of 128 (S/world=%lld)", (long long)S_r);
+  if (heads > 65535 || S >= (1ll << 31)) return fail(TL_ERR_UNSUPPORTED, "shape too large");
+  const int64_t row_elems = (int64_t)heads * D;
+  if (W > 1 && 2 * S * row_elems > c->max_M * c->max_H)
+    return fail(TL_ERR_INVALID, "gathered K/V (2*S*heads*D = %lld elements) exceed the comm capacity max_M*max_H = %lld",
+                (long long)(2 * S * row_elems), (long long)(c->max_M * c->max_H));
+  for (int i = 0; i < c->n_local; ++i) {
+    if (S * heads && (!Q[i] || !K[i] || !V[i] || !O[i])) return fail(TL_ERR_INVALID, "null pointer (rank slot %d)", i);
+    if (!aligned16(Q[i]) || !aligned16(K[i]) || !aligned16(V[i]) || !aligned16(O[i]))
+      return fail(TL_ERR_INVALID, "pointers must be 16-byte aligned");
+  }
+  if (S == 0 || heads == 0) return TL_OK;
+  const int64_t row_bytes = row_elems * 2;
+  StaticMap sm = StaticMap::make((int)S, W, (int)std::max<int64_t>(1, std::min<int64_t>(c->opt.comm_tile_rows, S_r)),
+                                 (int)c->opt.channels_per_rank);
+  if (W > 1 && sm.tiles_per_rank > kAgFlagStride)
+    return fail(TL_ERR_UNSUPPORTED, "too many producer tiles per rank (%d): raise comm_tile_rows", sm.tiles_per_rank);
+  TL_CUDA(cudaSetDevice(c->device));
+  const bool comm = W > 1;
+  const uint32_t epoch = comm ? ++c->ag_epoch : 0;
+  const int bank = epoch & 1;
+
+  AttnParams* pp = new AttnParams;
+  AttnParams& p = *pp;
+  memset(&p, 0, sizeof(p));
+  int cpr = c->opt.num_ctas > 0 ? (int)c->opt.num_ctas : c->sm_count / c->n_local;
+  if (cpr * c->n_local > c->sm_count) cpr = c->sm_count / c->n_local;
+  p.ctas_per_rank = std::max(1, cpr);
+  p.S = (int)S;
+  p.S_r = (int)S_r;
+  p.heads = heads;
+  p.world = W;
+  p.n_local = c->n_local;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.epoch = epoch;
+  p.timeout_ns = (uint64_t)c->opt.timeout_ms * 1000000ull;
+  p.diag = reinterpret_cast<Diag*>(c->ws[c->loopback ? 0 : c->rank] + c->lay.diag);
+  p.drop_rank = (int)c->opt.debug_drop_rank;
+  p.drop_index = (int)c->opt.debug_drop_notify;
+  p.tm_rows = sm.Tm;
+  p.tiles_per_rank = sm.tiles_per_rank;
+  p.tiles_per_channel = sm.tiles_per_channel;
+  p.copy_ctas = c->opt.copy_ctas > 0 ? (int)std::min<int64_t>(c->opt.copy_ctas, p.ctas_per_rank) : p.ctas_per_rank;
+  p.row_bytes = (int)row_bytes;
+  const size_t kv_bytes = (size_t)S * row_bytes;
+  if (comm)
+    for (int d = 0; d < W; ++d) {
+      p.kfull[d] = c->ws[d] + c->lay.xfull[bank];
+      p.vfull[d] = p.kfull[d] + kv_bytes;
+      p.ag_flags[d] = reinterpret_cast<uint32_t*>(c->ws[d] + c->lay.ag_flags);
+    }
+  for (int i = 0; i < c->n_local && st == TL_OK; ++i) {
+    const int r = local_rank_id(c, i);
+    AttnRank& ra = p.rk[i];
+    ra.rank = r;
+    ra.k_shard = reinterpret_cast<const uint8_t*>(K[i]);
+    ra.v_shard = reinterpret_cast<const uint8_t*>(V[i]);
+    const uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)row_bytes};
+    const uint64_t dq[3] = {(uint64_t)D, (uint64_t)heads, (uint64_t)S_r};
+    const uint64_t dkv[3] = {(uint64_t)D, (uint64_t)heads, (uint64_t)S};
+    const uint32_t box_in[3] = {64, 1, 128}, box_out[3] = {64, 1, 32};
+    const void* kf = comm ? (const void*)(c->ws[r] + c->lay.xfull[bank]) : K[i];
+    const void* vf = comm ? (const void*)(c->ws[r] + c->lay.xfull[bank] + kv_bytes) : V[i];
+    if ((st = make_tmap_nd(&ra.tm_q, Q[i], 3, dq, str, box_in)) != TL_OK) break;
+    if ((st = make_tmap_nd(&ra.tm_o, O[i], 3, dq, str, box_out)) != TL_OK) break;
+    if ((st = make_tmap_nd(&ra.tm_k, kf, 3, dkv, str, box_in)) != TL_OK) break;
+    if ((st = make_tmap_nd(&ra.tm_v, vf, 3, dkv, str, box_in)) != TL_OK) break;
+  }
+  if (st == TL_OK) {
+    auto kern = comm ? tl_attn_kernel<true> : tl_attn_kernel<false>;
+    const int smem = comm ? AttnLayout<true>::smem_request : AttnLayout<false>::smem_request;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) {
+      kern<<<p.n_local * p.ctas_per_rank, 256, smem, stream>>>(p);
+      e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "attention launch: %s", cudaGetErrorString(e));
+  }
+  delete pp;
+  return st;
+}
+}  // namespace
+
+extern "C" {
+
+tl_status tl_sp_attention(tl_comm_t c, const void* Q, const void* K, const void* V, void* O, int64_t S, int heads,
+                          int head_dim, float scale, void* stream) {
+  if (c && c->loopback) return fail(TL_ERR_STATE, "loopback comm: use tl_sp_attention_loopback");
+  return attn_impl(c, &Q, &K, &V, &O, S, heads, head_dim, scale, (cudaStream_t)stream);
+}
+
+tl_status tl_sp_attention_loopback(tl_comm_t c, const void* const* Q, const void* const* K, const void* const* V,
+                                   void* const* O, int64_t S, int heads, int head_dim, float scale, void* stream) {
+  if (!c || !c->loopback) return fail(TL_ERR_STATE, "not a loopback comm");
+  if (!Q || !K || !V || !O) return fail(TL_ERR_INVALID, "null pointer array");
+  return attn_impl(c, Q, K, V, O, S, heads, head_dim, scale, (cudaStream_t)stream);
 }
 
 }  // extern "C"
