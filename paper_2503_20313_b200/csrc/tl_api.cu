@@ -142,7 +142,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0;
+          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 0;
 };
 
 struct OptDesc {
@@ -165,6 +165,7 @@ const OptDesc kOpts[] = {
     {"ag_binding", &Options::ag_binding, 0, 1},
     {"dma_tile_rows", &Options::dma_tile_rows, 0, 1 << 20},
     {"debug_mode", &Options::debug_mode, 0, 2},
+    {"attn_poly", &Options::attn_poly, 0, 8},
 };
 
 }  // namespace
@@ -1244,23 +1245,28 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
     ra.rank = r;
     ra.k_shard = reinterpret_cast<const uint8_t*>(K[i]);
     ra.v_shard = reinterpret_cast<const uint8_t*>(V[i]);
+    ra.o = reinterpret_cast<uint8_t*>(O[i]);
     const uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)row_bytes};
     const uint64_t dq[3] = {(uint64_t)D, (uint64_t)heads, (uint64_t)S_r};
     const uint64_t dkv[3] = {(uint64_t)D, (uint64_t)heads, (uint64_t)S};
-    const uint32_t box_in[3] = {64, 1, 128}, box_out[3] = {64, 1, 32};
+    const uint32_t box_in[3] = {64, 1, 128};
     const void* kf = comm ? (const void*)(c->ws[r] + c->lay.xfull[bank]) : K[i];
     const void* vf = comm ? (const void*)(c->ws[r] + c->lay.xfull[bank] + kv_bytes) : V[i];
     if ((st = make_tmap_nd(&ra.tm_q, Q[i], 3, dq, str, box_in)) != TL_OK) break;
-    if ((st = make_tmap_nd(&ra.tm_o, O[i], 3, dq, str, box_out)) != TL_OK) break;
     if ((st = make_tmap_nd(&ra.tm_k, kf, 3, dkv, str, box_in)) != TL_OK) break;
     if ((st = make_tmap_nd(&ra.tm_v, vf, 3, dkv, str, box_in)) != TL_OK) break;
   }
   if (st == TL_OK) {
-    auto kern = comm ? tl_attn_kernel<true> : tl_attn_kernel<false>;
+    // fraction of exponentials on the FMA pipe: every attn_poly-th pair (0 = all on MUFU)
+    const int pm = (int)c->opt.attn_poly;
+    auto kern = comm ? (pm >= 8 ? tl_attn_kernel<true, 8> : pm >= 4 ? tl_attn_kernel<true, 4>
+                        : pm >= 2 ? tl_attn_kernel<true, 2> : tl_attn_kernel<true, 0>)
+                     : (pm >= 8 ? tl_attn_kernel<false, 8> : pm >= 4 ? tl_attn_kernel<false, 4>
+                        : pm >= 2 ? tl_attn_kernel<false, 2> : tl_attn_kernel<false, 0>);
     const int smem = comm ? AttnLayout<true>::smem_request : AttnLayout<false>::smem_request;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) {
-      kern<<<p.n_local * p.ctas_per_rank, 256, smem, stream>>>(p);
+      kern<<<p.n_local * p.ctas_per_rank, kAttnThreads, smem, stream>>>(p);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "attention launch: %s", cudaGetErrorString(e));

@@ -4,17 +4,28 @@
 // size for communication part is simply divide KVCache sequence length (S) by the total number of
 // ranks ... For computation part, the tile size is different").
 //
-// Persistent CTAs (one per SM) loop over (head, 128-query) tiles; per tile the KV sequence is walked
-// in 128-token blocks, own shard first then the other ranks' in ring order (expected arrival):
-//   warp 0      TMA producer: Q tile once, then K / V blocks (2-stage ring); AG mode first waits the
-//               flags of the producer tiles holding the block's tokens (consumer_tile_wait).
-//   warp 1      MMA: S_j = Q K_j^T (tcgen05 128x128x128 into one of two TMEM S buffers), then
-//               O += P_j V_j (P from smem, V MN-major) once the softmax published P_j.
-//   warp 2      TMEM allocator (S0 | S1 | O = 3 x 128 fp32 columns).
-//   warp 3      AG copy role (W > 1): bulk-copies this rank's K and V producer tiles to every rank.
-//   warps 4-7   online softmax, one query row per thread: row max, exp2, row sum, lazy O rescale
-//               (only when the row max grew), P -> smem (bf16, 128B-swizzled K-major), final 1/l and
-//               the O store.
+// Persistent CTAs (one per SM) loop over work units = (head, two 128-query tiles A and B).  Both
+// tiles share every K/V block the producer stages, and their softmaxes ping-pong against the tensor
+// core: while warpgroup A turns S_A(j) into P_A(j), the MMA warp runs P_B(j-1).V and Q_B.K_j^T, and
+// the other way round.  KV blocks (128 tokens) are walked own shard first, then the other ranks'
+// in ring order (expected arrival order of the gathered shards).
+//   warps 0-3   softmax + epilogue of tile A (one query row per thread = one TMEM lane);
+//   warps 4-7   same for tile B;
+//   warp 8      TMA producer: Q_A, Q_B once per unit, then K and V blocks (separate 2-stage rings);
+//               AG mode first waits the flags of the producer tiles holding the block's tokens;
+//   warp 9      MMA issuer: S_X = Q_X K^T (smem x smem), O_X += P_X V (P from TMEM, V MN-major);
+//   warp 10     TMEM allocator + AG copy role (W > 1): bulk-copies this rank's K and V producer
+//               tiles to every rank, then releases the tile's flag there;
+//   warp 11     idle.
+// TMEM (512 columns): S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).  P_X(j) is written
+// as packed bf16 over the first 64 columns of S_X(j) (in place; tcgen05 MMAs execute in issue order,
+// so S_X(j+1) only overwrites it after P_X(j).V has consumed it).
+// Online softmax in the log2 domain with a lazily updated row max: the running max m is only
+// raised when a row's block max exceeds it by more than kRescaleThresh (then O and l are rescaled);
+// otherwise P = 2^(s*c - m) <= 2^kRescaleThresh stays finite and exact up to rounding, and the
+// final O / l is unchanged because O and l carry the same stale m.  A fraction of the exponentials
+// is evaluated on the FMA pipe (Cody-Waite + minimax cubic, rel. err 1e-4 < bf16's 2^-9) to offload
+// the 16/clk/SM MUFU unit (measured, tools/mma_probe.cu).
 #pragma once
 #include "tl_params.h"
 #include "tl_primitives.cuh"
@@ -26,7 +37,7 @@ struct alignas(64) AttnRank {
   CUtensorMap tm_q;   // [S_r][heads][128] of this rank, 64 x 1 x 128 boxes
   CUtensorMap tm_k;   // [S][heads][128] gathered K (or the shard itself when world == 1)
   CUtensorMap tm_v;   // [S][heads][128] gathered V
-  CUtensorMap tm_o;   // [S_r][heads][128] output, 64 x 1 x 32 boxes
+  uint8_t* o;         // [S_r][heads][128] output
   const uint8_t* k_shard;
   const uint8_t* v_shard;
   int rank;
@@ -46,14 +57,16 @@ struct alignas(64) AttnParams {
   int drop_rank, drop_index;
 };
 
-constexpr int kAttnQ = 0;                        // Q: 2 halves (d 0-63, 64-127) x [128 rows][128 B]
-constexpr int kAttnKV = 32768;                   // 2 stages x (K 32 KB + V 32 KB)
-constexpr int kAttnP = kAttnKV + 2 * 65536;      // P: 2 halves (kv 0-63, 64-127) x [128][128 B]; O staging
-constexpr int kAttnCopy = kAttnP + 32768;        // AG copy staging (2 x 16 KB)
+constexpr int kAttnThreads = 384;
+constexpr float kRescaleThresh = 8.f;
+constexpr int kAttnQ = 0;                  // Q_A, Q_B: 2 x (2 halves (d 0-63, 64-127) x [128 rows][128 B])
+constexpr int kAttnK = 65536;              // K ring: 2 x 32 KB
+constexpr int kAttnV = kAttnK + 65536;     // V ring: 2 x 32 KB (MN-major operand: [kv][d] halves)
+constexpr int kAttnCopy = kAttnV + 65536;  // AG copy staging (2 x 16 KB)
 template <bool kAG>
 struct AttnLayout {
   static constexpr int off_bar = kAttnCopy + (kAG ? 2 * 16384 : 0);
-  static constexpr int n_bars = 16;
+  static constexpr int n_bars = 24;
   static constexpr int off_tmem = off_bar + n_bars * 8;
   static constexpr int smem_request = off_tmem + 16 + 1024;
 };
@@ -72,8 +85,70 @@ __device__ __forceinline__ void attn_wait_rows(const AttnParams& p, int rank, in
   }
 }
 
-template <bool kAG>
-__global__ void __launch_bounds__(256, 1) tl_attn_kernel(const __grid_constant__ AttnParams p) {
+// ---- packed fp32x2 helpers (FFMA2 / FADD2 on sm_100) and the FMA-pipe exp2
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// 2^x for x <= kRescaleThresh on the FMA pipe: x = n + f, n = rint(x) (1.5 * 2^23 trick), f in
+// [-0.5, 0.5]; 2^f by a minimax cubic (relative error 1.0e-4); 2^n added to the exponent field.
+// x is clamped at -126 (results below 2^-126 are ~0 against a row sum >= 1).
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
+  const float2 n = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fadd2(x, make_float2(-n.x, -n.y));
+  float2 q = ffma2(f, make_float2(0.05500893f, 0.05500893f), make_float2(0.24221098f, 0.24221098f));
+  q = ffma2(q, f, make_float2(0.69328293f, 0.69328293f));
+  q = ffma2(q, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%32], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31};" ::"r"(v[0]),
+      "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]),
+      "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]),
+      "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31]), "r"(taddr)
+      : "memory");
+}
+// O (+)= P . V with P [128 x 16] read from TMEM (packed bf16, K-major) and V from smem.
+__device__ __forceinline__ void mma_ts(uint32_t tmem_a, uint64_t bdesc, uint32_t tmem_d, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <bool kAG, int kPolyMod>
+__global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_constant__ AttnParams p) {
   using L = AttnLayout<kAG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -82,121 +157,159 @@ __global__ void __launch_bounds__(256, 1) tl_attn_kernel(const __grid_constant__
   const int cta = blockIdx.x % p.ctas_per_rank;
   const AttnRank& ra = p.rk[lr];
   const int rank = ra.rank;
-  const int nqb = p.S_r / 128, n_tiles = p.heads * nqb, n_kv = p.S / 128, bpr = p.S_r / 128;
+  const int nqb = p.S_r / 128, npairs = (nqb + 1) / 2, n_units = p.heads * npairs;
+  const int n_kv = p.S / 128, bpr = p.S_r / 128;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::off_bar);
-  uint64_t* q_full = bars + 0;
-  uint64_t* q_free = bars + 1;
-  uint64_t* kv_full = bars + 2;    // [2]
-  uint64_t* kv_empty = bars + 4;   // [2]
-  uint64_t* s_full = bars + 6;     // [2]
-  uint64_t* s_free = bars + 8;     // [2]
-  uint64_t* p_full = bars + 10;
-  uint64_t* o_done = bars + 11;
-  uint64_t* o_free = bars + 12;
-  uint64_t* cbar = bars + 13;      // [2]
+  uint64_t* q_full = bars + 0;    // [2] per tile
+  uint64_t* q_free = bars + 2;    // [2]
+  uint64_t* k_full = bars + 4;    // [2] per stage
+  uint64_t* k_empty = bars + 6;   // [2]
+  uint64_t* v_full = bars + 8;    // [2]
+  uint64_t* v_empty = bars + 10;  // [2]
+  uint64_t* s_full = bars + 12;   // [2] per tile
+  uint64_t* p_full = bars + 14;   // [2] per tile (4 warps)
+  uint64_t* o_full = bars + 16;   // [2] per tile
+  uint64_t* o_free = bars + 18;   // [2] per tile (4 warps)
+  uint64_t* cbar = bars + 20;     // [2] AG copy staging
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::off_tmem);
 
-  if (warp == 1 && lane == 0) {
-    ptx::mbar_init(q_full, 1);
-    ptx::mbar_init(q_free, 1);
+  if (warp == 9 && lane == 0) {
     for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&kv_full[i], 1);
-      ptx::mbar_init(&kv_empty[i], 1);
+      ptx::mbar_init(&q_full[i], 1);
+      ptx::mbar_init(&q_free[i], 1);
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&s_free[i], 4);
+      ptx::mbar_init(&p_full[i], 4);
+      ptx::mbar_init(&o_full[i], 1);
+      ptx::mbar_init(&o_free[i], 4);
       ptx::mbar_init(&cbar[i], 1);
     }
-    ptx::mbar_init(p_full, 4);
-    ptx::mbar_init(o_done, 1);
-    ptx::mbar_init(o_free, 4);
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc<1>(tmem_slot, 512);
+  if (warp == 10) ptx::tmem_alloc<1>(tmem_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;   // S0 at +0, S1 at +128, O at +256
-
-  if (warp == 0) {
+  const uint32_t tmem = *tmem_slot;
+  // registers: the softmax warpgroups hold a 128-column S row per thread; the control warpgroup
+  // (producer / MMA / copy) needs few.  384 x 168 >= 128 x 80 + 256 x 208.  (Issued inside each
+  // role's branch so that ptxas allocates every role's code under its own limit.)
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
+  }
+  if (warp == 8) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
-      int stage = 0, it = 0;
-      uint32_t phase = 0;
-      for (int tile = cta; tile < n_tiles; tile += p.ctas_per_rank, ++it) {
-        const int h = tile / nqb, qb = tile % nqb;   // query blocks innermost: concurrent CTAs share K/V
-        ptx::mbar_wait(q_free, (it & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(q_full, 32768);
-        ptx::tma_load_3d<1>(&ra.tm_q, q_full, smem + kAttnQ, 0, h, qb * 128);
-        ptx::tma_load_3d<1>(&ra.tm_q, q_full, smem + kAttnQ + 16384, 64, h, qb * 128);
-        for (int j = 0; j < n_kv; ++j) {
+      uint32_t g = 0, uses[2] = {0, 0};
+      for (int u = cta; u < n_units; u += p.ctas_per_rank) {
+        const int h = u / npairs, qb0 = 2 * (u % npairs);
+        const bool hasB = qb0 + 1 < nqb;   // query blocks innermost: concurrent CTAs share K/V
+        for (int x = 0; x < (hasB ? 2 : 1); ++x) {
+          ptx::mbar_wait(&q_free[x], (uses[x] & 1) ^ 1);
+          ++uses[x];
+          uint8_t* q = smem + kAttnQ + x * 32768;
+          ptx::mbar_arrive_expect_tx(&q_full[x], 32768);
+          ptx::tma_load_3d<1>(&ra.tm_q, &q_full[x], q, 0, h, (qb0 + x) * 128);
+          ptx::tma_load_3d<1>(&ra.tm_q, &q_full[x], q + 16384, 64, h, (qb0 + x) * 128);
+        }
+        for (int j = 0; j < n_kv; ++j, ++g) {
           const int kvb = (j + rank * bpr) % n_kv;   // own shard first, then r+1, r+2, ...
           if constexpr (kAG) attn_wait_rows(p, rank, kvb * 128, kvb * 128 + 128);
-          ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
-          uint8_t* kv = smem + kAttnKV + stage * 65536;
-          ptx::mbar_arrive_expect_tx(&kv_full[stage], 65536);
-          ptx::tma_load_3d<1>(&ra.tm_k, &kv_full[stage], kv, 0, h, kvb * 128);
-          ptx::tma_load_3d<1>(&ra.tm_k, &kv_full[stage], kv + 16384, 64, h, kvb * 128);
-          ptx::tma_load_3d<1>(&ra.tm_v, &kv_full[stage], kv + 32768, 0, h, kvb * 128);
-          ptx::tma_load_3d<1>(&ra.tm_v, &kv_full[stage], kv + 49152, 64, h, kvb * 128);
-          if (++stage == 2) stage = 0, phase ^= 1;
+          const int st = g & 1;
+          const uint32_t ph = (g >> 1) & 1;
+          ptx::mbar_wait(&k_empty[st], ph ^ 1);
+          uint8_t* k = smem + kAttnK + st * 32768;
+          ptx::mbar_arrive_expect_tx(&k_full[st], 32768);
+          ptx::tma_load_3d<1>(&ra.tm_k, &k_full[st], k, 0, h, kvb * 128);
+          ptx::tma_load_3d<1>(&ra.tm_k, &k_full[st], k + 16384, 64, h, kvb * 128);
+          ptx::mbar_wait(&v_empty[st], ph ^ 1);
+          uint8_t* v = smem + kAttnV + st * 32768;
+          ptx::mbar_arrive_expect_tx(&v_full[st], 32768);
+          ptx::tma_load_3d<1>(&ra.tm_v, &v_full[st], v, 0, h, kvb * 128);
+          ptx::tma_load_3d<1>(&ra.tm_v, &v_full[st], v + 16384, 64, h, kvb * 128);
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 9) {
     // ============================== MMA issuer ==============================
-    constexpr uint32_t idesc_s = ptx::idesc_bf16(128, 128);
-    constexpr uint32_t idesc_pv = ptx::idesc_bf16(128, 128) | (1u << 16);   // B (= V) MN-major
-    int stage = 0, prev_stage = 0, it = 0, js = 0, jp = 0;
-    uint32_t phase = 0;
-    for (int tile = cta; tile < n_tiles; tile += p.ctas_per_rank, ++it) {
-      ptx::mbar_wait(q_full, it & 1);
-      ptx::tc_fence_after();
-      for (int j = 0; j <= n_kv; ++j) {
-        if (j < n_kv) {   // S_j = Q K_j^T into S buffer js & 1
-          ptx::mbar_wait(&kv_full[stage], phase);
-          const int b = js & 1;
-          ptx::mbar_wait(&s_free[b], ((js >> 1) & 1) ^ 1);
-          ptx::tc_fence_after();
-          if (lane == 0) {
-            uint8_t* kv = smem + kAttnKV + stage * 65536;
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = ptx::idesc_bf16(128, 128);
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16(128, 128) | (1u << 16);   // B (= V) MN-major
+      uint32_t g = 0, q_uses[2] = {0, 0}, p_cnt[2] = {0, 0};
+      auto issue_s = [&](int x, int st) {   // S_X = Q_X K^T
+        const uint32_t q = ptx::smem_u32(smem + kAttnQ + x * 32768);
+        const uint32_t k = ptx::smem_u32(smem + kAttnK + st * 32768);
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-              const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(smem + kAttnQ + (ks >> 2) * 16384)) + 2 * (ks & 3);
-              const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(kv + (ks >> 2) * 16384)) + 2 * (ks & 3);
-              ptx::mma_bf16<1>(ad, bd, tmem + b * 128, idesc_s, ks > 0);
-            }
-            ptx::mma_commit<1>(&s_full[b]);
-            if (j == n_kv - 1) ptx::mma_commit<1>(q_free);
-          }
-          __syncwarp();
-          ++js;
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint64_t ad = ptx::smem_desc_sw128(q + (ks >> 2) * 16384) + 2 * (ks & 3);
+          const uint64_t bd = ptx::smem_desc_sw128(k + (ks >> 2) * 16384) + 2 * (ks & 3);
+          ptx::mma_bf16<1>(ad, bd, tmem + x * 128, idesc_s, ks > 0);
         }
-        if (j > 0) {      // O += P_{j-1} V_{j-1}
-          ptx::mbar_wait(p_full, jp & 1);
-          if (j == 1) ptx::mbar_wait(o_free, (it & 1) ^ 1);   // previous tile's O has been read out
-          ptx::tc_fence_after();
-          if (lane == 0) {
-            uint8_t* v = smem + kAttnKV + prev_stage * 65536 + 32768;
-            const uint64_t vd = ptx::smem_desc_sw128_lbo(ptx::smem_u32(v), 16384, 1024);
+        ptx::mma_commit<1>(&s_full[x]);
+      };
+      auto issue_pv = [&](int x, int st, bool first) {   // O_X (+)= P_X V
+        const uint64_t vd = ptx::smem_desc_sw128_lbo(ptx::smem_u32(smem + kAttnV + st * 32768), 16384, 1024);
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(smem + kAttnP + (kk >> 2) * 16384)) + 2 * (kk & 3);
-              ptx::mma_bf16<1>(ad, vd + 128 * kk, tmem + 256, idesc_pv, (j > 1 || kk > 0) ? 1u : 0u);
-            }
-            ptx::mma_commit<1>(&kv_empty[prev_stage]);
-            ptx::mma_commit<1>(o_done);
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + x * 128 + kk * 8, vd + 128 * kk, tmem + 256 + x * 128, idesc_pv, (!first || kk > 0) ? 1u : 0u);
+      };
+      auto wait_p = [&](int x) {
+        ptx::mbar_wait(&p_full[x], p_cnt[x] & 1);
+        ++p_cnt[x];
+        ptx::tc_fence_after();
+      };
+      for (int u = cta; u < n_units; u += p.ctas_per_rank) {
+        const bool hasB = 2 * (u % npairs) + 1 < nqb;
+        ptx::mbar_wait(&q_full[0], q_uses[0] & 1);
+        if (hasB) ptx::mbar_wait(&q_full[1], q_uses[1] & 1);
+        ptx::tc_fence_after();
+        const uint32_t g0 = g;
+        for (int j = 0; j <= n_kv; ++j) {
+          const int st = (g0 + j) & 1, pst = (g0 + j - 1) & 1;
+          if (j < n_kv) {
+            ptx::mbar_wait(&k_full[st], ((g0 + j) >> 1) & 1);
+            ptx::tc_fence_after();
+            issue_s(0, st);
           }
-          __syncwarp();
-          ++jp;
+          if (j > 0 && hasB) {   // P_B(j-1) V_{j-1}
+            wait_p(1);
+            if (j == 1) {
+              ptx::mbar_wait(&o_free[1], (q_uses[1] & 1) ^ 1);
+              ptx::tc_fence_after();
+            }
+            issue_pv(1, pst, j == 1);
+            ptx::mma_commit<1>(&v_empty[pst]);
+            if (j == n_kv) ptx::mma_commit<1>(&o_full[1]);
+          }
+          if (j < n_kv) {
+            if (hasB) issue_s(1, st);
+            ptx::mma_commit<1>(&k_empty[st]);
+            if (j == n_kv - 1) {
+              ptx::mma_commit<1>(&q_free[0]);
+              if (hasB) ptx::mma_commit<1>(&q_free[1]);
+            }
+            // P_A(j) V_j
+            ptx::mbar_wait(&v_full[st], ((g0 + j) >> 1) & 1);
+            wait_p(0);
+            if (j == 0) {
+              ptx::mbar_wait(&o_free[0], (q_uses[0] & 1) ^ 1);
+              ptx::tc_fence_after();
+            }
+            issue_pv(0, st, j == 0);
+            if (!hasB) ptx::mma_commit<1>(&v_empty[st]);
+            if (j == n_kv - 1) ptx::mma_commit<1>(&o_full[0]);
+          }
         }
-        if (j < n_kv) {
-          prev_stage = stage;
-          if (++stage == 2) stage = 0, phase ^= 1;
-        }
+        g += n_kv;
+        ++q_uses[0];
+        if (hasB) ++q_uses[1];
       }
     }
-  } else if (warp == 3) {
+  } else if (warp == 10) {
     // ============================== AG copy role (K and V shards) ==============================
     if constexpr (kAG) {
       if (lane == 0 && cta < p.copy_ctas) {
@@ -239,114 +352,115 @@ __global__ void __launch_bounds__(256, 1) tl_attn_kernel(const __grid_constant__
         }
       }
     }
-  } else if (warp >= 4) {
-    // ============================== online softmax + epilogue ==============================
-    const int ew = warp - 4;
-    const int row = ew * 32 + (int)lane;                 // query row inside the tile = TMEM lane
+  } else if (warp < 8) {
+    // ============================== online softmax + epilogue (tile x) ==============================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
+    const int x = warp / 4, ew = warp % 4;
     const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-    int it = 0, js = 0, jp = 0;
-    for (int tile = cta; tile < n_tiles; tile += p.ctas_per_rank, ++it) {
-      const int h = tile / nqb, qb = tile % nqb;
+    const uint32_t t_s = tmem + lane_base + x * 128, t_o = tmem + lane_base + 256 + x * 128;
+    const float c = p.scale_log2;
+    uint32_t s_cnt = 0, o_cnt = 0;
+    for (int u = cta; u < n_units; u += p.ctas_per_rank) {
+      const int h = u / npairs, qb = 2 * (u % npairs) + x;
+      if (qb >= nqb) continue;   // unit without a tile B
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kv; ++j) {
-        const int b = js & 1;
-        ptx::mbar_wait(&s_full[b], (js >> 1) & 1);
+        ptx::mbar_wait(&s_full[x], s_cnt & 1);
+        ++s_cnt;
         ptx::tc_fence_after();
-        float x[128];
+        float s[128];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tmem + lane_base + b * 128 + c * 32, x + 32 * c);
-        ptx::tmem_ld_wait_fence<128>(x);
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&s_free[b]);
-        ++js;
-        float mx = x[0];
+        for (int k = 0; k < 4; ++k) ptx::tmem_ld32(t_s + k * 32, s + 32 * k);
+        ptx::tmem_ld_wait_fence<128>(s);
+        // row max: 8 independent FMNMX3 chains
+        float mc[8];
 #pragma unroll
-        for (int i = 1; i < 128; ++i) mx = fmaxf(mx, x[i]);
-        const float m_new = fmaxf(m, mx * p.scale_log2);
-        const float alpha = ptx::ex2_approx(m - m_new);   // 0 on the first block (m = -inf)
-        float sum = 0.f;
+        for (int i = 0; i < 8; ++i) mc[i] = fmaxf(s[2 * i], s[2 * i + 1]);
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          x[i] = ptx::ex2_approx(fmaf(x[i], p.scale_log2, -m_new));
-          sum += x[i];
-        }
-        l = fmaf(l, alpha, sum);
-        m = m_new;
-        if (j > 0) {
-          // O of the previous blocks must be complete before it is rescaled and P overwritten
-          ptx::mbar_wait(o_done, (jp - 1) & 1);
-          ptx::tc_fence_after();
-          if (__any_sync(0xffffffffu, alpha != 1.f)) {   // lazy rescale: only when a row max grew
+        for (int i = 8; i < 64; ++i) mc[i & 7] = fmax3(mc[i & 7], s[2 * i], s[2 * i + 1]);
+        const float mx = fmax3(fmax3(mc[0], mc[1], mc[2]), fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7]));
+        const float m_blk = mx * c;
+        // lazy max: raise m only when the block max exceeds it by more than the threshold
+        const bool raise = m_blk > m + kRescaleThresh;
+        if (__any_sync(0xffffffffu, raise)) {
+          const float m_new = raise ? m_blk : m;
+          const float alpha = ptx::ex2_approx(m - m_new);   // 0 on the first block, 1 for rows kept
+          l *= alpha;
+          m = m_new;
+          if (j > 0) {   // O_X holds blocks < j (P_X(j-1).V completed before s_full fired)
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int k = 0; k < 4; ++k) {
               float o[32];
-              ptx::tmem_ld32(tmem + lane_base + 256 + c * 32, o);
+              ptx::tmem_ld32(t_o + k * 32, o);
               ptx::tmem_ld_wait_fence<32>(o);
 #pragma unroll
               for (int i = 0; i < 32; ++i) o[i] *= alpha;
-              ptx::tmem_st32(tmem + lane_base + 256 + c * 32, o);
+              ptx::tmem_st32(t_o + k * 32, o);
             }
-            ptx::tmem_st_wait();
           }
-        } else if (lane == 0) {
-          ptx::bulk_wait_read<0>();   // the previous tile's O stores have finished reading P's smem
         }
-        __syncwarp();
-        // P_j -> smem, bf16, K-major 128B-swizzled (two 64-column halves)
-        const uint32_t pbase = ptx::smem_u32(smem + kAttnP) + row * 128;
+        // P = 2^(s c - m), row sum, pack to bf16 pairs
+        const float2 cc = make_float2(c, c), mm = make_float2(-m, -m);
+        float2 acc[8];
 #pragma unroll
-        for (int c16 = 0; c16 < 16; ++c16) {
-          const float* q = x + 8 * c16;
-          ptx::st_shared_v4(pbase + (c16 >> 3) * 16384 + (((c16 & 7) ^ (row & 7)) << 4),
-                            ptx::pack_bf16x2(q[0], q[1]), ptx::pack_bf16x2(q[2], q[3]),
-                            ptx::pack_bf16x2(q[4], q[5]), ptx::pack_bf16x2(q[6], q[7]));
+        for (int i = 0; i < 8; ++i) acc[i] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int i2 = 0; i2 < 32; ++i2) {
+            const int i = hh * 32 + i2;
+            float2 v = ffma2(make_float2(s[2 * i], s[2 * i + 1]), cc, mm);
+            if (kPolyMod > 0 && (i % kPolyMod) == kPolyMod - 1) {
+              v = exp2_fma2(v);
+            } else {
+              v.x = ptx::ex2_approx(v.x);
+              v.y = ptx::ex2_approx(v.y);
+            }
+            acc[i & 7] = fadd2(acc[i & 7], v);
+            pk[i2] = cvt_bf16x2(v.x, v.y);
+          }
+          tmem_st32u(t_s + hh * 32, pk);
         }
-        ptx::fence_proxy_async_smem();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = fadd2(acc[i], acc[i + 4]);
+        acc[0] = fadd2(acc[0], acc[2]);
+        acc[1] = fadd2(acc[1], acc[3]);
+        acc[0] = fadd2(acc[0], acc[1]);
+        l += acc[0].x + acc[0].y;
+        ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(p_full);
-        ++jp;
+        if (lane == 0) ptx::mbar_arrive(&p_full[x]);
       }
-      // ---- epilogue: O / l -> bf16 -> TMA store (staged in this warp's quarter of P's smem)
-      ptx::mbar_wait(o_done, (jp - 1) & 1);
+      // ---- epilogue: O / l -> bf16 -> global (this thread's query row, 256 contiguous bytes)
+      ptx::mbar_wait(&o_full[x], o_cnt & 1);
+      ++o_cnt;
       ptx::tc_fence_after();
       const float inv = 1.f / l;
-      // staging = this warp's own rows of P's two halves (same addresses its P writes use)
-      uint8_t* stg = smem + kAttnP + ew * 4096;   // half h at + h * 16384: 32 rows x 128 B
+      uint8_t* orow = ra.o + ((size_t)(qb * 128 + ew * 32 + lane) * p.heads + h) * 256;
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int k = 0; k < 4; ++k) {
         float o[32];
-        ptx::tmem_ld32(tmem + lane_base + 256 + c * 32, o);
+        ptx::tmem_ld32(t_o + k * 32, o);
         ptx::tmem_ld_wait_fence<32>(o);
-        const uint32_t rb = ptx::smem_u32(stg + (c >> 1) * 16384) + lane * 128;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int c16 = (c & 1) * 4 + q;
-          ptx::st_shared_v4(rb + ((c16 ^ (lane & 7)) << 4), ptx::pack_bf16x2(o[8 * q] * inv, o[8 * q + 1] * inv),
-                            ptx::pack_bf16x2(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
-                            ptx::pack_bf16x2(o[8 * q + 4] * inv, o[8 * q + 5] * inv),
-                            ptx::pack_bf16x2(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
+        for (int v = 0; v < 4; ++v) {
+          const float* w = o + 8 * v;
+          uint4 val = make_uint4(cvt_bf16x2(w[0] * inv, w[1] * inv), cvt_bf16x2(w[2] * inv, w[3] * inv),
+                                 cvt_bf16x2(w[4] * inv, w[5] * inv), cvt_bf16x2(w[6] * inv, w[7] * inv));
+          *reinterpret_cast<uint4*>(orow + k * 64 + v * 16) = val;
         }
       }
       ptx::tc_fence_before();
-      ptx::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        ptx::mbar_arrive(o_free);
-        ptx::tma_store_3d(&ra.tm_o, stg, 0, h, qb * 128 + ew * 32);
-        ptx::tma_store_3d(&ra.tm_o, stg + 16384, 64, h, qb * 128 + ew * 32);
-        ptx::bulk_commit();
-      }
-      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&o_free[x]);
     }
-    if (lane == 0) ptx::bulk_wait<0>();
-    __syncwarp();
   }
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 10) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<1>(tmem, 512);
   }
