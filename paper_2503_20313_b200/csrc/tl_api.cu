@@ -142,7 +142,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 0;
+          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 4;
 };
 
 struct OptDesc {
@@ -1292,3 +1292,9 @@ tl_status tl_sp_attention_loopback(tl_comm_t c, const void* const* Q, const void
 }
 
 }  // extern "C"
+
+#ifdef TL_ATTN_TRACE
+extern "C" __attribute__((visibility("default"))) int tl_debug_attn_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, tl::g_attn_trace, sizeof(tl::g_attn_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif

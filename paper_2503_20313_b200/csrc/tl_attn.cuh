@@ -33,6 +33,17 @@
 
 namespace tl {
 
+#ifdef TL_ATTN_TRACE
+// Phase timestamps (clock64) of CTA 0's first unit, first 64 KV blocks: [slot][j][4]; slots 0/1 =
+// softmax warp 0 / 4 (tiles A / B), 2 = MMA waits for P, 3 = MMA waits for K/V, 4 = producer.
+// Experiments only (tools/attn_trace.py).
+__device__ unsigned long long g_attn_trace[5 * 64 * 4];
+#define TL_TRACE(slot, j, k) \
+  do { if (cta == 0 && (j) < 64) g_attn_trace[((slot) * 64 + (j)) * 4 + (k)] = clock64(); } while (0)
+#else
+#define TL_TRACE(slot, j, k) do {} while (0)
+#endif
+
 struct alignas(64) AttnRank {
   CUtensorMap tm_q;   // [S_r][heads][128] of this rank, 64 x 1 x 128 boxes
   CUtensorMap tm_k;   // [S][heads][128] gathered K (or the shard itself when world == 1)
@@ -147,6 +158,110 @@ __device__ __forceinline__ void mma_ts(uint32_t tmem_a, uint64_t bdesc, uint32_t
       : "memory");
 }
 
+// mbarrier parity wait without a suspend-time hint: ~30 clk quicker hand-off than the hinted
+// try_wait in tl_ptx.cuh (tools/wake_probe.cu); used on the S -> softmax -> P -> MMA chain.
+__device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = ptx::smem_u32(bar);
+  uint32_t ok = 0;
+  uint64_t t0 = 0;
+  for (uint32_t n = 0;; ++n) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (n == 0) t0 = ptx::globaltimer();
+    else if ((n & 0x3FFu) == 0 && ptx::globaltimer() - t0 > 20000000000ull) __trap();
+  }
+}
+
+// Warp-collective issue: every lane of the MMA warp runs the loop with warp-uniform operands (so
+// descriptors stay in uniform registers, no per-MMA waterfall), one elected lane issues.
+__device__ __forceinline__ void mma_ss_elect(uint64_t adesc, uint64_t bdesc, uint32_t tmem_d, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ts_elect(uint32_t tmem_a, uint64_t bdesc, uint32_t tmem_d, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// The 8 K=16 steps of one 128x128x128 product in one asm block: descriptors advance inside PTX
+// (uniform datapath), one elect.  S: A = Q (K-major, +32 B per step within a 64-column half,
+// +16 KB per half), B = K (same).  PV: A = P in TMEM (+8 columns per step), B = V (MN-major,
+// +2 KB per step).
+__device__ __forceinline__ void mma_s8_elect(uint64_t adesc, uint64_t bdesc, uint32_t tmem_d, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 a4, %1, 1024;\n\tadd.s64 a5, %1, 1026;\n\tadd.s64 a6, %1, 1028;\n\tadd.s64 a7, %1, 1030;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "add.s64 b4, %2, 1024;\n\tadd.s64 b5, %2, 1026;\n\tadd.s64 b6, %2, 1028;\n\tadd.s64 b7, %2, 1030;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, 1;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pv8_elect(uint32_t tmem_a, uint64_t bdesc, uint32_t tmem_d, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 b1, b2, b3, b4, b5, b6, b7;\n\t.reg .b32 t1, t2, t3, t4, t5, t6, t7;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.s64 b1, %2, 128;\n\tadd.s64 b2, %2, 256;\n\tadd.s64 b3, %2, 384;\n\tadd.s64 b4, %2, 512;\n\t"
+      "add.s64 b5, %2, 640;\n\tadd.s64 b6, %2, 768;\n\tadd.s64 b7, %2, 896;\n\t"
+      "add.s32 t1, %1, 8;\n\tadd.s32 t2, %1, 16;\n\tadd.s32 t3, %1, 24;\n\tadd.s32 t4, %1, 32;\n\t"
+      "add.s32 t5, %1, 40;\n\tadd.s32 t6, %1, 48;\n\tadd.s32 t7, %1, 56;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t1], b1, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t2], b2, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t3], b3, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t4], b4, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t5], b5, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t6], b6, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t7], b7, %3, 1;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Half of P.V: 4 K=16 steps (64 KV rows); half 1 starts at P column 32 and V row 64.
+__device__ __forceinline__ void mma_pv4_elect(uint32_t tmem_a, uint64_t bdesc, uint32_t tmem_d, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 t1, t2, t3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.s64 b1, %2, 128;\n\tadd.s64 b2, %2, 256;\n\tadd.s64 b3, %2, 384;\n\t"
+      "add.s32 t1, %1, 8;\n\tadd.s32 t2, %1, 16;\n\tadd.s32 t3, %1, 24;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t1], b1, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t2], b2, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t3], b3, %3, 1;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          ptx::smem_u32(bar))
+      : "memory");
+}
+
 template <bool kAG, int kPolyMod>
 __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_constant__ AttnParams p) {
   using L = AttnLayout<kAG>;
@@ -172,6 +287,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
   uint64_t* o_full = bars + 16;   // [2] per tile
   uint64_t* o_free = bars + 18;   // [2] per tile (4 warps)
   uint64_t* cbar = bars + 20;     // [2] AG copy staging
+  uint64_t* p_half = bars + 22;   // [2] per tile: first 64 KV columns of P written (4 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::off_tmem);
 
   if (warp == 9 && lane == 0) {
@@ -187,6 +303,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
       ptx::mbar_init(&o_full[i], 1);
       ptx::mbar_init(&o_free[i], 4);
       ptx::mbar_init(&cbar[i], 1);
+      ptx::mbar_init(&p_half[i], 4);
     }
     ptx::fence_mbar_init();
   }
@@ -204,29 +321,33 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
   if (warp == 8) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
-      uint32_t g = 0, uses[2] = {0, 0};
-      for (int u = cta; u < n_units; u += p.ctas_per_rank) {
-        const int h = u / npairs, qb0 = 2 * (u % npairs);
-        const bool hasB = qb0 + 1 < nqb;   // query blocks innermost: concurrent CTAs share K/V
-        for (int x = 0; x < (hasB ? 2 : 1); ++x) {
-          ptx::mbar_wait(&q_free[x], (uses[x] & 1) ^ 1);
-          ++uses[x];
+      uint32_t g = 0, uses = 0;
+      for (int u = cta; u < n_units; u += p.ctas_per_rank, ++uses) {
+        const int h = u / npairs, qb0 = 2 * (u % npairs);   // query blocks innermost: concurrent CTAs share K/V
+        // a unit without a tile B (odd query-block count) recomputes tile A as B and drops it
+        for (int x = 0; x < 2; ++x) {
+          const int qb = min(qb0 + x, nqb - 1);
+          ptx::mbar_wait(&q_free[x], (uses & 1) ^ 1);
           uint8_t* q = smem + kAttnQ + x * 32768;
           ptx::mbar_arrive_expect_tx(&q_full[x], 32768);
-          ptx::tma_load_3d<1>(&ra.tm_q, &q_full[x], q, 0, h, (qb0 + x) * 128);
-          ptx::tma_load_3d<1>(&ra.tm_q, &q_full[x], q + 16384, 64, h, (qb0 + x) * 128);
+          ptx::tma_load_3d<1>(&ra.tm_q, &q_full[x], q, 0, h, qb * 128);
+          ptx::tma_load_3d<1>(&ra.tm_q, &q_full[x], q + 16384, 64, h, qb * 128);
         }
         for (int j = 0; j < n_kv; ++j, ++g) {
           const int kvb = (j + rank * bpr) % n_kv;   // own shard first, then r+1, r+2, ...
           if constexpr (kAG) attn_wait_rows(p, rank, kvb * 128, kvb * 128 + 128);
           const int st = g & 1;
           const uint32_t ph = (g >> 1) & 1;
+          if (u == cta) TL_TRACE(4, j, 0);
           ptx::mbar_wait(&k_empty[st], ph ^ 1);
+          if (u == cta) TL_TRACE(4, j, 1);
           uint8_t* k = smem + kAttnK + st * 32768;
           ptx::mbar_arrive_expect_tx(&k_full[st], 32768);
           ptx::tma_load_3d<1>(&ra.tm_k, &k_full[st], k, 0, h, kvb * 128);
           ptx::tma_load_3d<1>(&ra.tm_k, &k_full[st], k + 16384, 64, h, kvb * 128);
+          if (u == cta) TL_TRACE(4, j, 2);
           ptx::mbar_wait(&v_empty[st], ph ^ 1);
+          if (u == cta) TL_TRACE(4, j, 3);
           uint8_t* v = smem + kAttnV + st * 32768;
           ptx::mbar_arrive_expect_tx(&v_full[st], 32768);
           ptx::tma_load_3d<1>(&ra.tm_v, &v_full[st], v, 0, h, kvb * 128);
@@ -236,77 +357,69 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
     }
   } else if (warp == 9) {
     // ============================== MMA issuer ==============================
-    if (lane == 0) {
+    // Whole warp runs the loop with uniform operands, one elected lane issues (no per-MMA
+    // waterfall).  Issue order per KV block j:  S_A(j) | P_B(j-1).V_{j-1}, S_B(j) | P_A(j).V_j, so
+    // softmax A(j) overlaps P_B(j-1).V and S_B(j), softmax B(j) overlaps P_A(j).V and S_A(j+1).
+    // S_X(j+1) is issued after P_X(j).V (tcgen05 MMAs execute in issue order), which protects
+    // P_X(j) in TMEM.  (Two issuing warps were measured no faster: tools/attn_trace.py.)
+    {
       constexpr uint32_t idesc_s = ptx::idesc_bf16(128, 128);
       constexpr uint32_t idesc_pv = ptx::idesc_bf16(128, 128) | (1u << 16);   // B (= V) MN-major
-      uint32_t g = 0, q_uses[2] = {0, 0}, p_cnt[2] = {0, 0};
+      uint32_t g = 0, uses = 0, p_cnt[2] = {0, 0};
+      (void)uses;
       auto issue_s = [&](int x, int st) {   // S_X = Q_X K^T
-        const uint32_t q = ptx::smem_u32(smem + kAttnQ + x * 32768);
-        const uint32_t k = ptx::smem_u32(smem + kAttnK + st * 32768);
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const uint64_t ad = ptx::smem_desc_sw128(q + (ks >> 2) * 16384) + 2 * (ks & 3);
-          const uint64_t bd = ptx::smem_desc_sw128(k + (ks >> 2) * 16384) + 2 * (ks & 3);
-          ptx::mma_bf16<1>(ad, bd, tmem + x * 128, idesc_s, ks > 0);
-        }
-        ptx::mma_commit<1>(&s_full[x]);
+        mma_s8_elect(ptx::smem_desc_sw128(ptx::smem_u32(smem + kAttnQ + x * 32768)),
+                     ptx::smem_desc_sw128(ptx::smem_u32(smem + kAttnK + st * 32768)), tmem + x * 128, idesc_s);
+        commit_elect(&s_full[x]);
       };
-      auto issue_pv = [&](int x, int st, bool first) {   // O_X (+)= P_X V
+      // O_X (+)= P_X V in two halves: the first 64 KV rows start as soon as the softmax has written
+      // the first half of P (p_half), overlapping the exponentials of the second half.
+      auto pv = [&](int x, int st, bool first) {
         const uint64_t vd = ptx::smem_desc_sw128_lbo(ptx::smem_u32(smem + kAttnV + st * 32768), 16384, 1024);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tmem + x * 128 + kk * 8, vd + 128 * kk, tmem + 256 + x * 128, idesc_pv, (!first || kk > 0) ? 1u : 0u);
-      };
-      auto wait_p = [&](int x) {
-        ptx::mbar_wait(&p_full[x], p_cnt[x] & 1);
+        mbar_wait_fast(&p_half[x], p_cnt[x] & 1);
+        ptx::tc_fence_after();
+        mma_pv4_elect(tmem + x * 128, vd, tmem + 256 + x * 128, idesc_pv, first ? 0u : 1u);
+        mbar_wait_fast(&p_full[x], p_cnt[x] & 1);
         ++p_cnt[x];
         ptx::tc_fence_after();
+        mma_pv4_elect(tmem + x * 128 + 32, vd + 512, tmem + 256 + x * 128, idesc_pv, 1u);
       };
-      for (int u = cta; u < n_units; u += p.ctas_per_rank) {
-        const bool hasB = 2 * (u % npairs) + 1 < nqb;
-        ptx::mbar_wait(&q_full[0], q_uses[0] & 1);
-        if (hasB) ptx::mbar_wait(&q_full[1], q_uses[1] & 1);
+      for (int u = cta; u < n_units; u += p.ctas_per_rank, ++uses) {
+        ptx::mbar_wait(&q_full[0], uses & 1);
+        ptx::mbar_wait(&q_full[1], uses & 1);
+        ptx::mbar_wait(&k_full[g & 1], (g >> 1) & 1);
         ptx::tc_fence_after();
-        const uint32_t g0 = g;
-        for (int j = 0; j <= n_kv; ++j) {
-          const int st = (g0 + j) & 1, pst = (g0 + j - 1) & 1;
-          if (j < n_kv) {
-            ptx::mbar_wait(&k_full[st], ((g0 + j) >> 1) & 1);
-            ptx::tc_fence_after();
-            issue_s(0, st);
+        issue_s(0, g & 1);
+        for (int j = 0; j < n_kv; ++j, ++g) {
+          const int st = g & 1;
+          const uint32_t ph = (g >> 1) & 1;
+          if (j > 0) {   // P_B(j-1) V_{j-1}
+            pv(1, st ^ 1, j == 1);
+            commit_elect(&v_empty[st ^ 1]);
           }
-          if (j > 0 && hasB) {   // P_B(j-1) V_{j-1}
-            wait_p(1);
-            if (j == 1) {
-              ptx::mbar_wait(&o_free[1], (q_uses[1] & 1) ^ 1);
-              ptx::tc_fence_after();
-            }
-            issue_pv(1, pst, j == 1);
-            ptx::mma_commit<1>(&v_empty[pst]);
-            if (j == n_kv) ptx::mma_commit<1>(&o_full[1]);
+          issue_s(1, st);   // K_j was waited before S_A(j)
+          commit_elect(&k_empty[st]);
+          if (j == n_kv - 1) {
+            commit_elect(&q_free[0]);
+            commit_elect(&q_free[1]);
           }
-          if (j < n_kv) {
-            if (hasB) issue_s(1, st);
-            ptx::mma_commit<1>(&k_empty[st]);
-            if (j == n_kv - 1) {
-              ptx::mma_commit<1>(&q_free[0]);
-              if (hasB) ptx::mma_commit<1>(&q_free[1]);
-            }
-            // P_A(j) V_j
-            ptx::mbar_wait(&v_full[st], ((g0 + j) >> 1) & 1);
-            wait_p(0);
-            if (j == 0) {
-              ptx::mbar_wait(&o_free[0], (q_uses[0] & 1) ^ 1);
-              ptx::tc_fence_after();
-            }
-            issue_pv(0, st, j == 0);
-            if (!hasB) ptx::mma_commit<1>(&v_empty[st]);
-            if (j == n_kv - 1) ptx::mma_commit<1>(&o_full[0]);
+          // waits that are normally already satisfied go before the P_A wait, so that
+          // P_A(j) -> P_A(j).V -> S_A(j+1) issues back to back
+          if (u == cta) TL_TRACE(3, j, 2);
+          ptx::mbar_wait(&v_full[st], ph);
+          if (j + 1 < n_kv) ptx::mbar_wait(&k_full[st ^ 1], ((g + 1) >> 1) & 1);
+          if (j == 0) {
+            ptx::mbar_wait(&o_free[0], (uses & 1) ^ 1);
+            ptx::mbar_wait(&o_free[1], (uses & 1) ^ 1);
           }
+          pv(0, st, j == 0);
+          if (j == n_kv - 1) commit_elect(&o_full[0]);
+          if (j + 1 < n_kv) issue_s(0, st ^ 1);   // S_A(j+1)
         }
-        g += n_kv;
-        ++q_uses[0];
-        if (hasB) ++q_uses[1];
+        // drain: P_B(n-1) V_{n-1}
+        pv(1, (g - 1) & 1, n_kv == 1);
+        commit_elect(&v_empty[(g - 1) & 1]);
+        commit_elect(&o_full[1]);
       }
     }
   } else if (warp == 10) {
@@ -362,12 +475,26 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
     uint32_t s_cnt = 0, o_cnt = 0;
     for (int u = cta; u < n_units; u += p.ctas_per_rank) {
       const int h = u / npairs, qb = 2 * (u % npairs) + x;
-      if (qb >= nqb) continue;   // unit without a tile B
+      const bool store = qb < nqb;   // a duplicated tile B (odd query-block count) is not stored
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kv; ++j) {
-        ptx::mbar_wait(&s_full[x], s_cnt & 1);
+        const bool tr = u == cta && lane == 0 && ew == 0;
+        if (tr) TL_TRACE(x, j, 0);
+        mbar_wait_fast(&s_full[x], s_cnt & 1);
         ++s_cnt;
         ptx::tc_fence_after();
+        if (tr) TL_TRACE(x, j, 1);
+#ifdef TL_ATTN_TRACE
+        if (p.drop_index == 12345) {   // MMA-chain-only experiment: no softmax work
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::mbar_arrive(&p_half[x]);
+            ptx::mbar_arrive(&p_full[x]);
+          }
+          continue;
+        }
+#endif
         float s[128];
 #pragma unroll
         for (int k = 0; k < 4; ++k) ptx::tmem_ld32(t_s + k * 32, s + 32 * k);
@@ -380,6 +507,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
         for (int i = 8; i < 64; ++i) mc[i & 7] = fmax3(mc[i & 7], s[2 * i], s[2 * i + 1]);
         const float mx = fmax3(fmax3(mc[0], mc[1], mc[2]), fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7]));
         const float m_blk = mx * c;
+        if (tr) TL_TRACE(x, j, 2);
         // lazy max: raise m only when the block max exceeds it by more than the threshold
         const bool raise = m_blk > m + kRescaleThresh;
         if (__any_sync(0xffffffffu, raise)) {
@@ -421,6 +549,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
             pk[i2] = cvt_bf16x2(v.x, v.y);
           }
           tmem_st32u(t_s + hh * 32, pk);
+          if (hh == 0) {   // release the first half of P to the MMA warp
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&p_half[x]);
+          }
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[i] = fadd2(acc[i], acc[i + 4]);
@@ -431,6 +565,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
+        if (tr) TL_TRACE(x, j, 3);
         if (lane == 0) ptx::mbar_arrive(&p_full[x]);
       }
       // ---- epilogue: O / l -> bf16 -> global (this thread's query row, 256 contiguous bytes)
@@ -438,18 +573,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
       ++o_cnt;
       ptx::tc_fence_after();
       const float inv = 1.f / l;
-      uint8_t* orow = ra.o + ((size_t)(qb * 128 + ew * 32 + lane) * p.heads + h) * 256;
+      if (store) {
+        uint8_t* orow = ra.o + ((size_t)(qb * 128 + ew * 32 + lane) * p.heads + h) * 256;
 #pragma unroll 1
-      for (int k = 0; k < 4; ++k) {
-        float o[32];
-        ptx::tmem_ld32(t_o + k * 32, o);
-        ptx::tmem_ld_wait_fence<32>(o);
+        for (int k = 0; k < 4; ++k) {
+          float o[32];
+          ptx::tmem_ld32(t_o + k * 32, o);
+          ptx::tmem_ld_wait_fence<32>(o);
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const float* w = o + 8 * v;
-          uint4 val = make_uint4(cvt_bf16x2(w[0] * inv, w[1] * inv), cvt_bf16x2(w[2] * inv, w[3] * inv),
-                                 cvt_bf16x2(w[4] * inv, w[5] * inv), cvt_bf16x2(w[6] * inv, w[7] * inv));
-          *reinterpret_cast<uint4*>(orow + k * 64 + v * 16) = val;
+          for (int v = 0; v < 4; ++v) {
+            const float* w = o + 8 * v;
+            uint4 val = make_uint4(cvt_bf16x2(w[0] * inv, w[1] * inv), cvt_bf16x2(w[2] * inv, w[3] * inv),
+                                   cvt_bf16x2(w[4] * inv, w[5] * inv), cvt_bf16x2(w[6] * inv, w[7] * inv));
+            *reinterpret_cast<uint4*>(orow + k * 64 + v * 16) = val;
+          }
         }
       }
       ptx::tc_fence_before();
