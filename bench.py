@@ -294,6 +294,30 @@ def main():
     e2e_val = (f1 + f2) * W / (e2e_ms * 1e-3) / 1e12
     e2e_match = bool(torch.equal(hout[0], out.cpu()))   # same input as the device-resident run, bitwise
 
+    # PCIe alone (explains e2e): one step's H2D / D2H copies by themselves, and both at once
+    def copy_ms(h2d, d2h, reps=5):
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(pipe.s_in)
+            if h2d:
+                with torch.cuda.stream(pipe.s_in):
+                    pipe.x[0].copy_(hin[0], non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(pipe.s_out):
+                    pipe.s_out.wait_event(a)
+                    hout[0].copy_(pipe.out[0], non_blocking=True)
+                pipe.s_in.wait_stream(pipe.s_out)
+            b.record(pipe.s_in)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return sorted(ts)[len(ts) // 2]
+    pcie = {"h2d_ms": round(copy_ms(True, False), 4), "d2h_ms": round(copy_ms(False, True), 4),
+            "both_ms": round(copy_ms(True, True), 4)}
+    pcie["h2d_gbs"] = round(pipe.bytes_in / pcie["h2d_ms"] / 1e6, 1)
+    pcie["d2h_gbs"] = round(pipe.bytes_out / pcie["d2h_ms"] / 1e6, 1)
+
     # ---- non-overlapped NCCL + cuBLAS baseline (same inputs, same protocol)
     base = None
     if not args.no_baseline:
@@ -417,7 +441,8 @@ def main():
                 "h2d_bytes_per_step": pipe.bytes_in, "d2h_bytes_per_step": pipe.bytes_out,
                 "api": "tl_mlp_forward via paper_2503_20313_b200.pipeline.MLPPipeline (pinned host X shard in, "
                        "output back, every step; copies overlap the previous/next step's layer)",
-                "output_matches_device_run": e2e_match},
+                "output_matches_device_run": e2e_match,
+                "pcie_alone": pcie},
         "gpu_launches": 2 * args.steps,
         "clocks": clk,
         "parity": parity,

@@ -1020,6 +1020,7 @@ tl_status moe_gemm_rs_impl(tl_comm* c, const void* const* Zg, const int32_t* con
   if (topk > c->max_topk)
     return fail(TL_ERR_UNSUPPORTED, "topk=%d exceeds the comm's max_topk=%d (tl_comm_create_ex)", topk, c->max_topk);
   if (M > c->max_M || H > c->max_H) return fail(TL_ERR_INVALID, "M/H exceed comm capacity");
+  if ((M / W) * (H / 8) >= (1ll << 31)) return fail(TL_ERR_UNSUPPORTED, "M/world * H/8 >= 2^31");
   for (int i = 0; i < c->n_local; ++i)
     if (!Zg[i] || !rows[i] || !offs[i] || !topk_w[i] || !W2[i] || !out[i] || !aligned16(Zg[i]) || !aligned16(W2[i]) ||
         !aligned16(out[i]))
@@ -1100,7 +1101,7 @@ tl_status moe_gemm_rs_impl(tl_comm* c, const void* const* Zg, const int32_t* con
     a.epoch = epoch;
     a.timeout_ns = p.timeout_ns;
     a.diag = p.diag;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((M_r * (H / 8) + 255) / 256,
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((M_r * (H / 8) + 511) / 512,
                                                                   8ll * c->sm_count / c->n_local));
     tl_moe_reduce_kernel<<<dim3(blocks, c->n_local), 256, 0, stream>>>(a);
     cudaError_t e = cudaGetLastError();

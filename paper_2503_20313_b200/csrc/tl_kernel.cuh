@@ -665,6 +665,54 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
 //   sched[j]    tiles ordered by the producer tile their last token lives in (expected arrival).
 // Every rank builds identical tables from the identical routing: no communication.
 constexpr int kMoeThreads = 1024;
+constexpr int kMoeLoadBatch = 16;   // routed entries in flight per lane (one memory latency per batch)
+
+// Exclusive scan of one int per thread over the 1024-thread block; *total = sum.  s32: 32 ints of
+// smem.  Called by every thread (contains block barriers).
+__device__ __forceinline__ int moe_block_scan(int v, int* s32, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s32[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = s32[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    s32[lane] = w;
+  }
+  __syncthreads();
+  const int base = warp ? s32[warp - 1] : 0;
+  *total = s32[31];
+  __syncthreads();   // s32 may be reused by the next call
+  return base + x - v;
+}
+
+// Lanes of the warp holding the same key (0 <= key < 2^nbits): nbits ballots.  Replaces
+// __match_any_sync, whose MATCH.ANY serialises (measured: the table kernel spent most of its 25 us
+// in 2 x 16 matches per warp).
+__device__ __forceinline__ unsigned moe_peers(int key, int nbits) {
+  unsigned m = 0xffffffffu;
+  for (int b = 0; b < nbits; ++b) {
+    const bool bit = (key >> b) & 1;
+    const unsigned v = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? v : ~v;
+  }
+  return m;
+}
+
+// Dynamic tile-centric mapping tables from the routing, one CTA: stable counting sort of
+// the n = M * topk routed entries by expert (entry order inside an expert = (token, slot) order),
+// padded group offsets, per-tile {expert, first token, last token} and the tile schedule.
+// Every serial step of the first version (expert and bucket scans by one thread, one global-load
+// latency per 32 entries) is a block-wide scan or a batched load here.
 __global__ void __launch_bounds__(kMoeThreads, 1)
     tl_moe_tables_kernel(const int* __restrict__ ids, int n, int topk, int E, int BM, int M_r, int Tm,
                          int key_shift, int* rows, int* offs, int* tab, int* sched, int max_tiles, int* err) {
@@ -674,72 +722,93 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
   int* soffs = cnt + E;          // [E + 1]
   int* keys = soffs + E + 1;     // [max_tiles]
   int* bcnt = keys + max_tiles;  // [kMoeThreads] bucket counts -> starts
+  __shared__ int s32[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // each warp owns one contiguous chunk of the routed entries (stable order = chunk order)
   const int chunk = (n + 31) / 32, lo = warp * chunk, hi = min(lo + chunk, n);
+  const int nbits = 32 - __clz(E);   // keys e + 1 in [0, E]
   for (int x = tid; x < 32 * E; x += kMoeThreads) wcnt[x] = 0;
   __syncthreads();
-  for (int i0 = lo; i0 < hi; i0 += 32) {       // pass 1: per-warp expert histogram (warp-private smem)
-    const int i = i0 + lane;
-    int e = i < hi ? ids[i] : -1;
-    if (e >= E || (i < hi && e < 0)) {
-      atomicExch(err, 1);
-      e = -1;
+  for (int b0 = lo; b0 < hi; b0 += 32 * kMoeLoadBatch) {   // pass 1: per-warp expert histogram
+    int ev[kMoeLoadBatch];
+#pragma unroll
+    for (int u = 0; u < kMoeLoadBatch; ++u) {
+      const int i = b0 + u * 32 + lane;
+      ev[u] = i < hi ? __ldg(ids + i) : -1;
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    if (e >= 0 && (peers & ((1u << lane) - 1u)) == 0) wcnt[warp * E + e] += __popc(peers);
-    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kMoeLoadBatch; ++u) {
+      const int i = b0 + u * 32 + lane;
+      int e = ev[u];
+      if (e >= E || (i < hi && e < 0)) {
+        atomicExch(err, 1);
+        e = -1;
+      }
+      if (e >= 0) atomicAdd(&wcnt[warp * E + e], 1);   // counts only: order is irrelevant here
+    }
   }
   __syncthreads();
-  // padded group offsets, then per-warp starting positions (exclusive scan over warps per expert)
-  if (tid == 0) {
-    int o = 0;
-    for (int e = 0; e < E; ++e) {
-      int c = 0;
-      for (int w = 0; w < 32; ++w) c += wcnt[w * E + e];
-      cnt[e] = c;
-      soffs[e] = o;
-      o += (c + BM - 1) / BM * BM;
-    }
-    soffs[E] = o;
-    tab[0] = o / BM;
+  // expert totals (parallel over experts), padded group offsets by a block scan (E <= 1024)
+  int my_cnt = 0;
+  if (tid < E) {
+    for (int w = 0; w < 32; ++w) my_cnt += wcnt[w * E + tid];
+    cnt[tid] = my_cnt;
   }
-  __syncthreads();
-  for (int e = tid; e < E; e += kMoeThreads) {
-    int run = soffs[e];
+  int padded_total = 0;
+  const int my_off = moe_block_scan(tid < E ? (my_cnt + BM - 1) / BM * BM : 0, s32, &padded_total);
+  if (tid < E) {
+    soffs[tid] = my_off;
+    offs[tid] = my_off;
+    int run = my_off;                           // per-warp starting positions of this expert
     for (int w = 0; w < 32; ++w) {
-      const int c = wcnt[w * E + e];
-      wcnt[w * E + e] = run;
+      const int c = wcnt[w * E + tid];
+      wcnt[w * E + tid] = run;
       run += c;
     }
+    for (int g = my_off + my_cnt; g < my_off + (my_cnt + BM - 1) / BM * BM; ++g) rows[g] = -1;   // padding
   }
-  for (int e = tid; e <= E; e += kMoeThreads) offs[e] = soffs[e];
-  __syncthreads();
-  for (int i0 = lo; i0 < hi; i0 += 32) {       // pass 2: place entries, stable inside each warp chunk
-    const int i = i0 + lane;
-    int e = i < hi ? ids[i] : -1;
-    if (e >= E) e = -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    const int lrank = __popc(peers & ((1u << lane) - 1u));
-    if (e >= 0) rows[wcnt[warp * E + e] + lrank] = i;
-    __syncwarp();
-    if (e >= 0 && lrank == 0) wcnt[warp * E + e] += __popc(peers);
-    __syncwarp();
+  if (tid == 0) {
+    soffs[E] = padded_total;
+    offs[E] = padded_total;
+    tab[0] = padded_total / BM;
   }
-  for (int e = 0; e < E; ++e)
-    for (int g = soffs[e] + cnt[e] + tid; g < soffs[e + 1]; g += kMoeThreads) rows[g] = -1;
   __syncthreads();
-  const int n_tiles = soffs[E] / BM;
+  for (int b0 = lo; b0 < hi; b0 += 32 * kMoeLoadBatch) {   // pass 2: place entries, stable per chunk
+    int ev[kMoeLoadBatch];
+#pragma unroll
+    for (int u = 0; u < kMoeLoadBatch; ++u) {
+      const int i = b0 + u * 32 + lane;
+      ev[u] = i < hi ? __ldg(ids + i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kMoeLoadBatch; ++u) {
+      const int i = b0 + u * 32 + lane;
+      int e = ev[u];
+      if (e >= E) e = -1;
+      const unsigned peers = moe_peers(e + 1, nbits);   // lanes routing to the same expert
+      const int lrank = __popc(peers & ((1u << lane) - 1u));
+      if (e >= 0) rows[wcnt[warp * E + e] + lrank] = i;
+      __syncwarp();
+      if (e >= 0 && lrank == 0) wcnt[warp * E + e] += __popc(peers);
+      __syncwarp();
+    }
+  }
+  __syncthreads();   // rows[] written by other threads is read below (same CTA: bar.sync orders it)
+  const int n_tiles = padded_total / BM;
   // tile table + schedule key: (producer tile of the tile's last token) >> key_shift, then expert,
   // so tiles of one expert that become ready together run together (their B blocks shared in L2)
   const int n_keys = ((M_r + Tm - 1) / Tm + (1 << key_shift) - 1) >> key_shift;
   const int n_buckets = min(n_keys * E, kMoeThreads);
-  for (int x = tid; x < kMoeThreads; x += kMoeThreads) bcnt[x] = 0;
+  bcnt[tid] = 0;
   __syncthreads();
   for (int t = tid; t < n_tiles; t += kMoeThreads) {
     const int g0 = t * BM;
-    int e = 0;
-    while (soffs[e + 1] <= g0) ++e;
+    int a = 0, b = E - 1;                       // expert e with soffs[e] <= g0 < soffs[e + 1]
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (soffs[mid] <= g0) a = mid; else b = mid - 1;
+    }
+    const int e = a;
     const int last = min(g0 + BM, soffs[e] + cnt[e]) - 1;
     const int tlo = rows[g0] / topk, thi = rows[last] / topk;
     tab[4 + 3 * t] = e;
@@ -750,17 +819,10 @@ __global__ void __launch_bounds__(kMoeThreads, 1)
     atomicAdd(&bcnt[keys[t]], 1);
   }
   __syncthreads();
-  if (tid == 0) {
-    int o = 0;
-    for (int b = 0; b < n_buckets; ++b) {
-      const int c = bcnt[b];
-      bcnt[b] = o;
-      o += c;
-    }
-  }
-  __syncthreads();
+  int n_sched = 0;
+  const int start = moe_block_scan(bcnt[tid], s32, &n_sched);
   if (tid < n_buckets) {
-    int o = bcnt[tid];
+    int o = start;
     for (int t = 0; t < n_tiles; ++t)
       if (keys[t] == tid) sched[o++] = t;
   }
@@ -786,38 +848,59 @@ __global__ void __launch_bounds__(256) tl_moe_reduce_kernel(const __grid_constan
     flag_wait(a.flags[lr] + threadIdx.x, a.epoch, a.timeout_ns, a.diag, rank, 3, threadIdx.x, 0);
   __syncthreads();
   const int cpr = a.H / 8;                       // 16-byte chunks per row
-  const long long n = (long long)a.M_r * cpr;
+  const int n = a.M_r * cpr;                     // < 2^31 (validated on the host)
   const int terms = a.world * a.topk;
   const size_t slot_stride = (size_t)a.M_r * a.topk * a.H;   // elements between source-rank slots
-  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
-    const int t = (int)(i / cpr), c = (int)(i % cpr) * 8;
-    const uint16_t* base = a.staging[lr] + (size_t)t * a.topk * a.H + c;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j0 = 0; j0 < terms; j0 += 8) {      // 8 independent 16-byte loads in flight
-      uint4 q[8];
+  const int stride = gridDim.x * 256;
+  // two chunks per thread and four terms per group: 8 independent 16-byte loads in flight
+  for (int i0 = blockIdx.x * 256 + threadIdx.x; i0 < n; i0 += 2 * stride) {
+    const uint16_t* base[2];
+    uint16_t* dst[2];
+    bool ok[2];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+    for (int v = 0; v < 2; ++v) {
+      const int i = i0 + v * stride;
+      ok[v] = i < n;
+      const int t = ok[v] ? i / cpr : 0, c = ok[v] ? (i - t * cpr) * 8 : 0;
+      base[v] = a.staging[lr] + (size_t)t * a.topk * a.H + c;
+      dst[v] = a.out[lr] + (size_t)t * a.H + c;
+    }
+    float acc[2][8];
+#pragma unroll
+    for (int v = 0; v < 2; ++v)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[v][e] = 0.f;
+    for (int j0 = 0; j0 < terms; j0 += 4) {
+      uint4 q[2][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
         const int j = j0 + u;
-        if (j < terms) {
-          const int s = j / a.topk, k = j - s * a.topk;   // ascending source rank, then slot
-          q[u] = ptx::ld_global_v4(base + s * slot_stride + (size_t)k * a.H);
-        }
+        const int s = j / a.topk, k = j - s * a.topk;   // ascending source rank, then slot
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+          if (ok[v] && j < terms) q[v][u] = ptx::ld_global_v4(base[v] + s * slot_stride + (size_t)k * a.H);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 4; ++u) {
         if (j0 + u < terms) {
-          const uint32_t w4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            acc[2 * e] += __uint_as_float(w4[e] << 16);
-            acc[2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+          for (int v = 0; v < 2; ++v) {
+            const uint32_t w4[4] = {q[v][u].x, q[v][u].y, q[v][u].z, q[v][u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              acc[v][2 * e] += __uint_as_float(w4[e] << 16);
+              acc[v][2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+            }
           }
         }
       }
     }
-    *reinterpret_cast<uint4*>(a.out[lr] + (size_t)t * a.H + c) =
-        make_uint4(ptx::pack_bf16x2(acc[0], acc[1]), ptx::pack_bf16x2(acc[2], acc[3]),
-                   ptx::pack_bf16x2(acc[4], acc[5]), ptx::pack_bf16x2(acc[6], acc[7]));
+#pragma unroll
+    for (int v = 0; v < 2; ++v)
+      if (ok[v])
+        *reinterpret_cast<uint4*>(dst[v]) =
+            make_uint4(ptx::pack_bf16x2(acc[v][0], acc[v][1]), ptx::pack_bf16x2(acc[v][2], acc[v][3]),
+                       ptx::pack_bf16x2(acc[v][4], acc[v][5]), ptx::pack_bf16x2(acc[v][6], acc[v][7]));
   }
 }
 

@@ -102,8 +102,11 @@ def run(name, S, H, I, E, topk, W=1):
 
 
 if __name__ == "__main__":
+    only = set(sys.argv[1:])          # e.g. MoE-4 MoE-1_rank_of_tp8 (default: all)
     out = []
     for n, (S, H, I, E, k) in SHAPES.items():
-        out.append(run(n, S, H, I, E, k, W=1))
-        out.append(run(n + "_rank_of_tp8", S, H, I, E, k, W=8))
-    json.dump(out, open("gpurun_out/moe_bench.json", "w"), indent=1)
+        for name, W in ((n, 1), (n + "_rank_of_tp8", 8)):
+            if not only or name in only:
+                out.append(run(name, S, H, I, E, k, W=W))
+    if not only:
+        json.dump(out, open("gpurun_out/moe_bench.json", "w"), indent=1)
