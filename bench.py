@@ -2,7 +2,7 @@
 """Benchmark of the TileLink B200 TP-MLP layer (BASELINE.json metric: TP-MLP layer TFLOPS & ms,
 vs non-overlapped NCCL + cuBLAS, % of roofline).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload mlp|moe|attention]
 
 N = 1 : the LLaMA-7B MLP layer (M=8192 tokens, H=4096, I=11008, gated SiLU) on one B200, W = 1
         (AG and RS degenerate to identities), through tl_mlp_forward's two kernels.
@@ -178,8 +178,16 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-loopback", action="store_true")
     ap.add_argument("--no-baseline", action="store_true")
+    ap.add_argument("--workload", default="mlp", choices=["mlp", "moe", "attention"],
+                    help="mlp = the north-star TP-MLP layer (default); moe / attention = SURVEY NEXT-3 / NEXT-4 "
+                         "(bench_workloads.py), same JSON contract")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.workload != "mlp":
+        import bench_workloads as BW
+        if args.impl == "reference":
+            return BW.run_reference(args)
+        return (BW.run_moe if args.workload == "moe" else BW.run_attention)(args, (Clocks, peaks))
     if args.impl == "reference":
         return run_reference(args)
 

@@ -1,0 +1,506 @@
+"""bench.py --workload moe | attention: the SURVEY §8(f) rows built beyond the MLP (NEXT-3, NEXT-4),
+measured to the same contract as the MLP line (one JSON line from rank 0 with roofline, cpu_baseline,
+e2e, clocks, parity and a library baseline).
+
+  moe       : the paper's MoE-4 layer (S = 8192 tokens, H = 4096, I = 2048, E = 8, top-2),
+              both halves: tl_moe_ag_gemm (AG + Gather + GroupGEMM + SiLU*up, dynamic mapping P:422-431)
+              then tl_moe_gemm_rs (GroupGEMM + Scatter + TopK reduce + RS).
+  attention : the paper's Attn-1 shape (32 heads, head dim 128) at S = 16384, non-causal:
+              tl_sp_attention (AllGather K/V fused with a tcgen05 flash-attention forward).
+
+N = 1 runs one rank (AG / RS degenerate to identities); N > 1 runs under torchrun, one process
+per GPU, tensor / sequence parallel W = N over the IPC workspace.  Work per rank is the paper's
+sharding of a fixed layer (strong scaling).  Inputs are seeded synthetic tensors (tl_inputs), all
+larger than the 126 MB L2.  `--impl reference` times the fp64 oracle on bounded row samples.
+"""
+from __future__ import annotations
+
+import json
+import os
+import time
+
+MOE = {"name": "MoE-4", "S": 8192, "H": 4096, "I": 2048, "E": 8, "topk": 2}
+ATTN = {"name": "Attn-1", "S": 16384, "heads": 32, "D": 128}
+
+
+def moe_config(W):
+    c = dict(MOE)
+    c.update({"workload": f"moe4_tp{W}", "world": W, "act": "silu_mul", "routing": "uniform top-2 (seeded)",
+              "parallelism": f"tp{W}", "l2": "inputs larger than L2 (W1 256 MiB + W2 128 MiB + X 64 MiB)"})
+    return c
+
+
+def attn_config(W):
+    c = dict(ATTN)
+    c.update({"workload": f"attn1_s16k_sp{W}", "world": W, "causal": False, "parallelism": f"sp{W}",
+              "l2": "inputs larger than L2 (Q, K, V 128 MiB each)"})
+    return c
+
+
+def moe_flops(W):
+    """Routed-work FLOPs per rank: GEMM1 2*(S*topk)*H*(2*I/W) + GEMM2 2*(S*topk)*(I/W)*H (padding rows
+    of the grouped layout are not counted)."""
+    S, H, I, k = MOE["S"], MOE["H"], MOE["I"], MOE["topk"]
+    il = I // W
+    return 2 * S * k * H * 2 * il, 2 * S * k * il * H
+
+
+def attn_flops(W):
+    """Non-causal attention FLOPs per rank: QK^T and PV, 2 * 2 * S_r * S * heads * D."""
+    S, h, D = ATTN["S"], ATTN["heads"], ATTN["D"]
+    return 4 * (S // W) * S * h * D
+
+
+# ----------------------------------------------------------------------------- shared plumbing
+def _dist():
+    import torch
+    import torch.distributed as dist
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env > 1:
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return dist.get_rank(), dist.get_world_size(), True
+    torch.cuda.set_device(0)
+    return 0, 1, False
+
+
+def _timed(step, steps, warmup, barrier, stream, n_marks):
+    """Warm-up, then `steps` steps bracketed by barrier + synchronize; `step(i, ev)` records
+    `n_marks` events per step on `stream`.  Returns (total_ms, per-segment mean ms lists)."""
+    import torch
+    for i in range(warmup):
+        step(i, None)
+    barrier()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_marks)] for _ in range(steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    t0.record(stream)
+    for i in range(steps):
+        step(i, ev[i])
+    t1.record(stream)
+    barrier()
+    seg = [sum(e[j].elapsed_time(e[j + 1]) for e in ev) / steps for j in range(n_marks - 1)]
+    return t0.elapsed_time(t1), seg
+
+
+def _common(metric, value, unit, W, args, ms, config):
+    return {"metric": metric, "value": round(value, 2), "unit": unit, "n_gpus": W, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": config}
+
+
+# ----------------------------------------------------------------------------- MoE
+def _moe_inputs(W):
+    import tl_inputs as TI
+    S, H, I, E, k = MOE["S"], MOE["H"], MOE["I"], MOE["E"], MOE["topk"]
+    il = I // W
+    X = TI._randn((S, H), 0, 0)
+    ids = TI.moe_routing(S, E, k, seed=2)
+    wts = TI.moe_topk_weights(S, k, seed=4)
+    W1s = TI.moe_weights(E, 2 * il, H, W, seed=1)
+    W2s = TI.moe_down_weights(E, H, il, W, seed=3)
+    return X, ids, wts, W1s, W2s
+
+
+def _moe_oracle_tokens(X, ids, wts, W1s, W2s, toks):
+    """The oracle's TP MoE forward restricted to a token sample (tokens are independent, so this is the
+    exact result for them); returns [n, H] = sum over ranks of the sampled tokens' outputs."""
+    import numpy as np
+    import tl_inputs as TI
+    from oracle import tl_oracle as O
+    W = len(W1s)
+    Xs = [TI.to_f64(X[toks])]
+    outs = O.moe_forward(Xs, ids[toks].numpy(), wts[toks].numpy(), W1s, W2s, TI.ACT_SILU_MUL)
+    assert len(toks) % W == 0
+    return np.concatenate(outs, 0)
+
+
+def _moe_cpu_leg(X, ids, wts, W1s64, W2s64, seconds, W):
+    import numpy as np
+    f1, f2 = moe_flops(W)
+    per_tok = (f1 + f2) * W / MOE["S"]
+    rng = np.random.default_rng(1)
+    n = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        toks = np.sort(rng.choice(MOE["S"], 8 * W, replace=False))
+        _moe_oracle_tokens(X, ids, wts, W1s64, W2s64, toks)
+        n += len(toks)
+    dt = time.perf_counter() - t0
+    return {"value": round(per_tok * n / dt / 1e12, 6), "unit": "TFLOPS", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{n} random tokens of the MoE-4 layer through oracle.moe_forward (fp64, per-row loops; "
+                      f"tokens are independent, so the sample is exact for them), {dt:.1f} s"}
+
+
+def run_moe(args, helpers):
+    Clocks, peaks = helpers
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2503_20313_b200 as tl
+    import tl_inputs as TI
+    from paper_2503_20313_b200.bootstrap import max_over_ranks
+    from oracle import tl_oracle as O
+
+    rank, W, distributed = _dist()
+    dev = torch.cuda.current_device()
+    P_burst, P_sust, peak_src = peaks()
+    S, H, I, E, k = MOE["S"], MOE["H"], MOE["I"], MOE["E"], MOE["topk"]
+    il, Mr = I // W, S // W
+    X, ids, wts, W1s, W2s = _moe_inputs(W)
+    x = X[rank * Mr:(rank + 1) * Mr].contiguous().cuda()
+    ids_d, wts_d = ids.cuda(), wts.cuda()
+    w1, w2 = W1s[rank].cuda(), W2s[rank].cuda()
+    if distributed:
+        comm = tl.Comm.from_process_group(None, dev, S, H, max_topk=k)
+    else:
+        comm = tl.Comm.single(dev, S, H, max_topk=k)
+    R = tl.moe_capacity(comm, S, k, E)
+    Y = torch.empty(R, il, device="cuda", dtype=torch.bfloat16)
+    rows = torch.empty(R, device="cuda", dtype=torch.int32)
+    offs = torch.empty(E + 1, device="cuda", dtype=torch.int32)
+    out = torch.empty(Mr, H, device="cuda", dtype=torch.bfloat16)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(i, ev):
+        if ev:
+            ev[0].record(stream)
+        tl.moe_ag_gemm(comm, x, ids_d, w1, Y, rows, offs, act=tl.ACT_SILU_MUL, stream=stream)
+        if ev:
+            ev[1].record(stream)
+        tl.moe_gemm_rs(comm, Y, rows, offs, wts_d, w2, out, stream=stream)
+        if ev:
+            ev[2].record(stream)
+
+    clocks = Clocks(dev)
+    clocks.start()
+    time.sleep(0.3)
+    total, (k1, k2) = _timed(step, args.steps, args.warmup, barrier, stream, 3)
+    soak = time.perf_counter() + 1.0
+    while time.perf_counter() < soak:
+        for i in range(8):
+            step(i, None)
+        torch.cuda.synchronize()
+    clk = clocks.stop()
+    total, k1, k2 = max_over_ranks(total), max_over_ranks(k1), max_over_ranks(k2)
+    ms = total / args.steps
+    st, _ = comm.check()
+    f1, f2 = moe_flops(W)
+    value = (f1 + f2) * W / (ms * 1e-3) / 1e12
+    ach1 = f1 / (k1 * 1e-3) / 1e12
+    ach2 = f2 / (k2 * 1e-3) / 1e12
+
+    # parity on sampled tokens of this rank against the oracle
+    parity = None
+    if rank == 0:
+        toks = np.arange(0, Mr, max(1, Mr // 16))[:16]
+        toks = toks[:len(toks) - len(toks) % W] if W > 1 else toks
+        f = lambda L: [TI.to_f64(t) for t in L]
+        W1s64, W2s64 = f(W1s), f(W2s)
+        ref = _moe_oracle_tokens(X, ids, wts, W1s64, W2s64, toks)
+        got = out[torch.as_tensor(toks, device="cuda")].float().cpu().double().numpy()
+        parity = {"tokens": len(toks), "rel_fro": O.rel_frobenius(got, ref), "tol": 5e-3, "status": int(st)}
+
+    # e2e through the public API: X shard, routing and router weights in from pinned host memory,
+    # the layer, the output back to pinned host memory, every step (stream-ordered)
+    hx = x.cpu().pin_memory()
+    hids, hwts = ids.pin_memory(), wts.pin_memory()
+    hout = torch.empty(Mr, H, dtype=torch.bfloat16).pin_memory()
+    xe, ide, wte = torch.empty_like(x), torch.empty_like(ids_d), torch.empty_like(wts_d)
+
+    def e2e_step(i, ev):
+        if ev:
+            ev[0].record(stream)
+        xe.copy_(hx, non_blocking=True)
+        ide.copy_(hids, non_blocking=True)
+        wte.copy_(hwts, non_blocking=True)
+        tl.moe_ag_gemm(comm, xe, ide, w1, Y, rows, offs, act=tl.ACT_SILU_MUL, stream=stream)
+        tl.moe_gemm_rs(comm, Y, rows, offs, wte, w2, out, stream=stream)
+        hout.copy_(out, non_blocking=True)
+        if ev:
+            ev[1].record(stream)
+    e2e_total, _ = _timed(e2e_step, args.steps, args.warmup, barrier, stream, 2)
+    e2e_ms = max_over_ranks(e2e_total) / args.steps
+    e2e_bytes_in = hx.numel() * 2 + hids.numel() * 4 + hwts.numel() * 4
+
+    # library baseline: torch index gather + per-expert cuBLAS + silu*mul, per-expert cuBLAS + weighted
+    # index_add (+ NCCL all_gather / reduce_scatter for W > 1), same inputs, same protocol
+    flat = ids_d.flatten().long()
+    order = torch.argsort(flat, stable=True)
+    tok = order // k
+    counts = torch.bincount(flat, minlength=E).tolist()
+    wsorted = wts_d.flatten()[order].unsqueeze(1)
+    xg = torch.empty(S, H, device="cuda", dtype=torch.bfloat16)
+    part = torch.empty(S, H, device="cuda", dtype=torch.float32)
+    ob = torch.empty(Mr, H, device="cuda", dtype=torch.float32)
+
+    def base_step(i, ev):
+        if ev:
+            ev[0].record(stream)
+        if distributed:
+            dist.all_gather_into_tensor(xg, x)
+            src = xg
+        else:
+            src = x
+        xs = src.index_select(0, tok)
+        zs, o = [], 0
+        for e in range(E):
+            y = xs[o:o + counts[e]] @ w1[e].T
+            zs.append(torch.nn.functional.silu(y[:, :il]) * y[:, il:])
+            o += counts[e]
+        ps, o = [], 0
+        for e in range(E):
+            ps.append(zs[e] @ w2[e].T)
+            o += counts[e]
+        p = torch.cat(ps).float() * wsorted
+        part.zero_()
+        part.index_add_(0, tok, p)
+        if distributed:
+            dist.reduce_scatter_tensor(ob, part)
+        else:
+            ob.copy_(part)
+        if ev:
+            ev[1].record(stream)
+    b_total, _ = _timed(base_step, args.steps, args.warmup, barrier, stream, 2)
+    bms = max_over_ranks(b_total) / args.steps
+
+    cpu = None
+    if rank == 0 and not distributed:
+        f = lambda L: [TI.to_f64(t) for t in L]
+        cpu = _moe_cpu_leg(X, ids, wts, f(W1s), f(W2s), args.cpu_seconds, W)
+    line = _common("TP-MoE layer TFLOPS (MoE-4: AG+Gather+GroupGEMM+SiLU*up, GroupGEMM+Scatter+TopK+RS)",
+                   value, "TFLOPS", W, args, ms, moe_config(W))
+    line.update({
+        "tflops_per_gpu": round(value / W, 2),
+        "kernels_ms": {"moe_ag_gemm": round(k1, 4), "moe_gemm_rs": round(k2, 4)},
+        "roofline": {"bound": "tensor", "kernel": "tl_moe_ag_gemm call (routing-table kernel + gather GroupGEMM)",
+                     "achieved": round(ach1, 2), "peak": P_burst, "unit": "TFLOP/s", "frac": round(ach1 / P_burst, 4),
+                     "frac_sustained": round(ach1 / P_sust, 4), "peak_source": peak_src,
+                     "second_half": {"achieved": round(ach2, 2), "frac": round(ach2 / P_burst, 4)},
+                     "layer_frac": round(value / W / P_burst, 4), "traffic": None, "per_launch_flop": f1,
+                     "flop_note": "routed rows only (S*topk); expert groups padded to 256 rows add ~6 % MMA work"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round((f1 + f2) * W / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
+                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": e2e_bytes_in,
+                "d2h_bytes_per_step": hout.numel() * 2,
+                "api": "tl_moe_ag_gemm + tl_moe_gemm_rs (pinned host X shard, routing and router weights in, "
+                       "output back, every step, stream-ordered)"},
+        "gpu_launches": 5 * args.steps,
+        "clocks": clk,
+        "parity": parity,
+        "baseline_torch": {"impl": "torch index_select + per-expert cuBLAS + silu*mul + per-expert cuBLAS + "
+                                   "weighted index_add (+ NCCL all_gather / reduce_scatter for W > 1)",
+                           "ms_per_step": round(bms, 4), "value": round((f1 + f2) * W / (bms * 1e-3) / 1e12, 2),
+                           "unit": "TFLOPS", "speedup_ours": round(bms / ms, 4)},
+    })
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    comm.close()
+    if distributed:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- SP attention
+def _attn_oracle_rows(Q, K64, V64, rows):
+    """oracle.sp_attention on a sample of query rows (rows are independent) with the full K/V
+    (K64 / V64: the gathered K and V already converted to fp64 numpy)."""
+    import tl_inputs as TI
+    from oracle import tl_oracle as O
+    D = ATTN["D"]
+    return O.sp_attention([TI.to_f64(Q[rows])], [K64], [V64], D ** -0.5)[0]
+
+
+def run_attention(args, helpers):
+    Clocks, peaks = helpers
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2503_20313_b200 as tl
+    import tl_inputs as TI
+    from paper_2503_20313_b200.bootstrap import max_over_ranks
+    from oracle import tl_oracle as O
+
+    rank, W, distributed = _dist()
+    dev = torch.cuda.current_device()
+    P_burst, P_sust, peak_src = peaks()
+    S, h, D = ATTN["S"], ATTN["heads"], ATTN["D"]
+    Sr = S // W
+    Qs, Ks, Vs = TI.attention_inputs(S, h, D, W, seed=0)
+    q, kk, v = Qs[rank].cuda(), Ks[rank].cuda(), Vs[rank].cuda()
+    o = torch.empty_like(q)
+    if distributed:
+        comm = tl.Comm.from_process_group(None, dev, S, 2 * h * D)
+    else:
+        comm = tl.Comm.single(dev, S, 2 * h * D)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(i, ev):
+        if ev:
+            ev[0].record(stream)
+        tl.sp_attention(comm, q, kk, v, o, stream=stream)
+        if ev:
+            ev[1].record(stream)
+
+    clocks = Clocks(dev)
+    clocks.start()
+    time.sleep(0.3)
+    total, (k1,) = _timed(step, args.steps, args.warmup, barrier, stream, 2)
+    soak = time.perf_counter() + 1.0
+    while time.perf_counter() < soak:
+        for i in range(4):
+            step(i, None)
+        torch.cuda.synchronize()
+    clk = clocks.stop()
+    total, k1 = max_over_ranks(total), max_over_ranks(k1)
+    ms = total / args.steps
+    st, _ = comm.check()
+    fl = attn_flops(W)
+    value = fl * W / (ms * 1e-3) / 1e12
+    ach = fl / (k1 * 1e-3) / 1e12
+
+    parity = None
+    if rank == 0:
+        Q = torch.cat(Qs, 0)
+        K64, V64 = (TI.to_f64(torch.cat(L, 0)) for L in (Ks, Vs))
+        rws = np.arange(0, Sr, max(1, Sr // 8))[:8]
+        ref = _attn_oracle_rows(Q, K64, V64, rws)
+        got = o[torch.as_tensor(rws, device="cuda")].float().cpu().double().numpy()
+        parity = {"rows": len(rws), "rel_fro": O.rel_frobenius(got, ref), "tol": 5e-3, "status": int(st)}
+
+    hq, hk, hv = (t.pin_memory() for t in (Qs[rank], Ks[rank], Vs[rank]))
+    ho = torch.empty_like(hq).pin_memory()
+    qe, ke, ve = torch.empty_like(q), torch.empty_like(kk), torch.empty_like(v)
+
+    def e2e_step(i, ev):
+        if ev:
+            ev[0].record(stream)
+        qe.copy_(hq, non_blocking=True)
+        ke.copy_(hk, non_blocking=True)
+        ve.copy_(hv, non_blocking=True)
+        tl.sp_attention(comm, qe, ke, ve, o, stream=stream)
+        ho.copy_(o, non_blocking=True)
+        if ev:
+            ev[1].record(stream)
+    e2e_total, _ = _timed(e2e_step, args.steps, args.warmup, barrier, stream, 2)
+    e2e_ms = max_over_ranks(e2e_total) / args.steps
+
+    # library baseline: NCCL all_gather of K/V (W > 1) + torch SDPA (cuDNN / flash backends)
+    kg = torch.empty(S, h, D, device="cuda", dtype=torch.bfloat16)
+    vg = torch.empty_like(kg)
+    qt = q.transpose(0, 1).unsqueeze(0)
+
+    def base_step(i, ev):
+        if ev:
+            ev[0].record(stream)
+        if distributed:
+            dist.all_gather_into_tensor(kg, kk)
+            dist.all_gather_into_tensor(vg, v)
+            kt, vt = kg, vg
+        else:
+            kt, vt = kk, v
+        torch.nn.functional.scaled_dot_product_attention(qt, kt.transpose(0, 1).unsqueeze(0),
+                                                         vt.transpose(0, 1).unsqueeze(0))
+        if ev:
+            ev[1].record(stream)
+    b_total, _ = _timed(base_step, args.steps, args.warmup, barrier, stream, 2)
+    bms = max_over_ranks(b_total) / args.steps
+
+    cpu = None
+    if rank == 0 and not distributed:
+        rng = np.random.default_rng(1)
+        n, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < args.cpu_seconds:
+            rws = np.sort(rng.choice(S, 64, replace=False))
+            _attn_oracle_rows(Q, K64, V64, rws)
+            n += len(rws)
+        dt = time.perf_counter() - t0
+        cpu = {"value": round(4 * S * h * D * n / dt / 1e12, 6), "unit": "TFLOPS", "cores": os.cpu_count(),
+               "kind": "oracle", "sample": f"{n} random query rows (all 32 heads, full K/V) through "
+                                           f"oracle.sp_attention (fp64 numpy), {dt:.1f} s"}
+    line = _common("SP attention TFLOPS (Attn-1: 32 heads x 128, S = 16384, non-causal; AllGather K/V + "
+                   "flash attention)", value, "TFLOPS", W, args, ms, attn_config(W))
+    line.update({
+        "tflops_per_gpu": round(value / W, 2),
+        "kernels_ms": {"sp_attention": round(k1, 4)},
+        "roofline": {"bound": "tensor", "kernel": "tl_attn_kernel (AG K/V + flash attention)",
+                     "achieved": round(ach, 2), "peak": P_burst, "unit": "TFLOP/s", "frac": round(ach / P_burst, 4),
+                     "frac_sustained": round(ach / P_sust, 4), "peak_source": peak_src, "traffic": None,
+                     "per_launch_flop": fl,
+                     "note": "MUFU exp2 (16/clk/SM) co-limits: 128x128 scores per 2 x 128^3 MMA FLOPs"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(fl * W / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
+                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": 3 * hq.numel() * 2,
+                "d2h_bytes_per_step": ho.numel() * 2,
+                "api": "tl_sp_attention (pinned host Q/K/V shards in, O back, every step, stream-ordered)"},
+        "gpu_launches": args.steps,
+        "clocks": clk,
+        "parity": parity,
+        "baseline_torch": {"impl": "torch SDPA (cuDNN/flash backend as torch selects) (+ NCCL all_gather "
+                                   "of K and V for W > 1)", "ms_per_step": round(bms, 4),
+                           "value": round(fl * W / (bms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
+                           "speedup_ours": round(bms / ms, 4)},
+    })
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    comm.close()
+    if distributed:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The oracle as it stands on the host cores, each step a bounded sample of the workload
+    (rank 0 only); same metric, unit and config as our arm."""
+    import numpy as np
+    import torch
+    import tl_inputs as TI
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    W = max(1, args.gpus)
+    rng = np.random.default_rng(0)
+    if args.workload == "moe":
+        X, ids, wts, W1s, W2s = _moe_inputs(W)
+        f = lambda L: [TI.to_f64(t) for t in L]
+        W1s, W2s = f(W1s), f(W2s)
+        f1, f2 = moe_flops(W)
+        per = (f1 + f2) * W / MOE["S"]
+        n_per = 8 * W
+        run = lambda: _moe_oracle_tokens(X, ids, wts, W1s, W2s, np.sort(rng.choice(MOE["S"], n_per, replace=False)))
+        metric = "TP-MoE layer TFLOPS (MoE-4: AG+Gather+GroupGEMM+SiLU*up, GroupGEMM+Scatter+TopK+RS)"
+        cfg, what = moe_config(W), f"{n_per} random tokens of the MoE-4 layer per step (oracle.moe_forward, fp64)"
+    else:
+        Qs, Ks, Vs = TI.attention_inputs(ATTN["S"], ATTN["heads"], ATTN["D"], W, seed=0)
+        Q = torch.cat(Qs, 0)
+        K64, V64 = (TI.to_f64(torch.cat(L, 0)) for L in (Ks, Vs))
+        per = 4 * ATTN["S"] * ATTN["heads"] * ATTN["D"]
+        n_per = 64
+        run = lambda: _attn_oracle_rows(Q, K64, V64, np.sort(rng.choice(ATTN["S"], n_per, replace=False)))
+        metric = ("SP attention TFLOPS (Attn-1: 32 heads x 128, S = 16384, non-causal; AllGather K/V + "
+                  "flash attention)")
+        cfg, what = attn_config(W), f"{n_per} random query rows per step (oracle.sp_attention, fp64)"
+    for _ in range(args.warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    dt = time.perf_counter() - t0
+    tflops = per * n_per * args.steps / dt / 1e12
+    line = _common(metric, tflops, "TFLOPS", args.gpus, args, dt / args.steps * 1e3, cfg)
+    line["value"] = round(tflops, 6)
+    line.update({"impl": "reference", "dtype": "f64",
+                 "cpu_baseline": {"value": round(tflops, 6), "unit": "TFLOPS", "cores": os.cpu_count(),
+                                  "kind": "oracle", "sample": what},
+                 "e2e": {"value": round(tflops, 6), "unit": "TFLOPS", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0}})
+    print(json.dumps(line), flush=True)
