@@ -1035,7 +1035,10 @@ tl_status moe_gemm_rs_impl(tl_comm* c, const void* const* Zg, const int32_t* con
   Params* pp = new Params;
   Params& p = *pp;
   fill_common(c, p);
-  const int nsub = (pair == 2 && c->opt.n_sub != 1 && (c->opt.n_sub == 2 || H >= 512)) ? 2 : 1;
+  // 256-wide tiles with a double-buffered accumulator by default: the scatter epilogue (the
+  // bottleneck of this GEMM) then overlaps the next tile's MMAs.  Measured on MoE-1..6
+  // (profiles/r01_moe_nsub_probe.log): equal or 1-8 % faster than 512-wide.
+  const int nsub = (pair == 2 && c->opt.n_sub == 2) ? 2 : 1;
   p.M = (int)R_cap;
   p.N_out = (int)H;
   p.K = (int)I_l;
