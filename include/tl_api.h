@@ -120,7 +120,9 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *                      2 = 512-wide (less L2 traffic, un-overlapped epilogue)
  *   "debug_mode"       overlap-ratio measurement: 0 normal, 1 computation only (no AG
  *                      copies or waits; results are garbage unless X_full already holds the data),
- *                      2 communication only (only the AG copy role runs) */
+ *                      2 communication only (only the AG copy role runs)
+ *   "attn_poly"        tl_sp_attention: every n-th pair of exponentials is evaluated on the FMA pipe
+ *                      (Cody-Waite + cubic) instead of MUFU (default 3; 0 = all on MUFU; 2,3,4,6,8) */
 tl_status tl_set_option(tl_comm_t comm, const char* key, int64_t value);
 tl_status tl_get_option(tl_comm_t comm, const char* key, int64_t* value);
 

@@ -142,7 +142,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 4;
+          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3;
 };
 
 struct OptDesc {
@@ -1263,10 +1263,13 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
   if (st == TL_OK) {
     // fraction of exponentials on the FMA pipe: every attn_poly-th pair (0 = all on MUFU)
     const int pm = (int)c->opt.attn_poly;
-    auto kern = comm ? (pm >= 8 ? tl_attn_kernel<true, 8> : pm >= 4 ? tl_attn_kernel<true, 4>
-                        : pm >= 2 ? tl_attn_kernel<true, 2> : tl_attn_kernel<true, 0>)
-                     : (pm >= 8 ? tl_attn_kernel<false, 8> : pm >= 4 ? tl_attn_kernel<false, 4>
-                        : pm >= 2 ? tl_attn_kernel<false, 2> : tl_attn_kernel<false, 0>);
+    auto pick = [&](auto k0, auto k2, auto k3, auto k4, auto k6, auto k8) {
+      return pm >= 8 ? k8 : pm >= 6 ? k6 : pm >= 4 ? k4 : pm == 3 ? k3 : pm >= 2 ? k2 : k0;
+    };
+    auto kern = comm ? pick(tl_attn_kernel<true, 0>, tl_attn_kernel<true, 2>, tl_attn_kernel<true, 3>,
+                            tl_attn_kernel<true, 4>, tl_attn_kernel<true, 6>, tl_attn_kernel<true, 8>)
+                     : pick(tl_attn_kernel<false, 0>, tl_attn_kernel<false, 2>, tl_attn_kernel<false, 3>,
+                            tl_attn_kernel<false, 4>, tl_attn_kernel<false, 6>, tl_attn_kernel<false, 8>);
     const int smem = comm ? AttnLayout<true>::smem_request : AttnLayout<false>::smem_request;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) {
