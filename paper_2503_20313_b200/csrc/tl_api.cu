@@ -458,9 +458,12 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   p.M_r = (int)M_r;
   p.epoch = epoch;
   p.m_blocks = (int)((M + 128 * pair - 1) / (128 * pair));
-  // MoE: 512-wide tiles whenever N fills them -- one gathered A stage then feeds twice the MMAs
+  // MoE: 512-wide tiles whenever one 256-wide tile does not cover N -- one gathered A stage then
+  // feeds twice the MMAs.  The row gathers, not the MMAs, bound this GEMM, so this wins even when
+  // the second sub-tile is partly empty (TP-8 rank shapes, I/W = 192: 1.3-1.5x; W = 1: 1.5-1.7x;
+  // profiles/r01_moe_nsub_probe.log).
   const int nsub = moe ? ((pair_of(c) == 2 && c->opt.n_sub != 1 &&
-                           (c->opt.n_sub == 2 || N_out >= (act != TL_ACT_NONE ? 256 : 512))) ? 2 : 1)
+                           (c->opt.n_sub == 2 || N_out > (act != TL_ACT_NONE ? 128 : 256))) ? 2 : 1)
                        : choose_nsub(c, M, N_out, K, act != TL_ACT_NONE);
   const int bn_out = (act ? 128 : 256) * nsub;
   p.n_blocks = (int)((N_out + bn_out - 1) / bn_out);
