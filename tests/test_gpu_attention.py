@@ -185,3 +185,23 @@ def test_attention_paper_shape_attn1_16k_sampled(tl):
         ref = O.sp_attention([q], [K64], [V64], D ** -0.5)[0]
         got = outs[r][torch.as_tensor(rows, device="cuda")].float().cpu().double().numpy()
         assert O.rel_frobenius(got, ref) < TOL
+
+
+def test_attention_bench_config_w1_sampled(tl):
+    """bench.py --workload attention at N = 1, exactly: Attn-1 heads (32 x 128), S = 16384, W = 1, the
+    bench's seeded inputs and comm; sampled query rows of every 2k-row block against the oracle
+    evaluated row by row over the full K/V."""
+    import bench_workloads as BW
+    S, heads, D = BW.ATTN["S"], BW.ATTN["heads"], BW.ATTN["D"]
+    Qs, Ks, Vs = TI.attention_inputs(S, heads, D, 1, seed=0)
+    comm = tl.Comm.single(0, S, 2 * heads * D)
+    q, k, v = Qs[0].cuda(), Ks[0].cuda(), Vs[0].cuda()
+    o = torch.empty_like(q)
+    tl.sp_attention(comm, q, k, v, o)
+    st, diag = comm.check()
+    assert st == 0, diag
+    rows = np.arange(0, S, 2048) + np.random.default_rng(3).integers(0, 2048, S // 2048)
+    K64, V64 = TI.to_f64(Ks[0]), TI.to_f64(Vs[0])
+    ref = O.sp_attention([TI.to_f64(Qs[0])[rows]], [K64], [V64], D ** -0.5)[0]
+    got = o[torch.as_tensor(rows, device="cuda")].float().cpu().double().numpy()
+    assert O.rel_frobenius(got, ref) < TOL

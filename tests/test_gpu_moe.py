@@ -162,3 +162,27 @@ def test_moe_layer_single_expert_matches_dense_mlp_kernels(tl):
     results, ref = _moe_layer(tl, W, M, H, I, E=1, topk=1)
     got = np.concatenate([o.float().cpu().double().numpy() for o in results[0]], 0)
     assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
+
+
+def test_moe_layer_bench_config_w1_sampled(tl):
+    """bench.py --workload moe at N = 1, exactly: MoE-4 (S = 8192, H = 4096, I = 2048, E = 8, top-2), both
+    halves, the bench's seeded inputs and comm; 32 sampled tokens against the oracle (tokens are
+    independent, so the token-sampled oracle is exact for them)."""
+    import bench_workloads as BW
+    S, H, I, E, k = (BW.MOE[n] for n in ("S", "H", "I", "E", "topk"))
+    X, ids, wts, W1s, W2s = BW._moe_inputs(1)
+    comm = tl.Comm.single(0, S, H, max_topk=k)
+    R = tl.moe_capacity(comm, S, k, E)
+    Y = torch.empty(R, I, device="cuda", dtype=torch.bfloat16)
+    rows = torch.empty(R, device="cuda", dtype=torch.int32)
+    offs = torch.empty(E + 1, device="cuda", dtype=torch.int32)
+    out = torch.empty(S, H, device="cuda", dtype=torch.bfloat16)
+    tl.moe_ag_gemm(comm, X.cuda(), ids.cuda(), W1s[0].cuda(), Y, rows, offs, act=tl.ACT_SILU_MUL)
+    tl.moe_gemm_rs(comm, Y, rows, offs, wts.cuda(), W2s[0].cuda(), out)
+    st, diag = comm.check()
+    assert st == 0, diag
+    toks = np.sort(np.random.default_rng(5).choice(S, 32, replace=False))
+    f = lambda L: [TI.to_f64(t) for t in L]
+    ref = BW._moe_oracle_tokens(X, ids, wts, f(W1s), f(W2s), toks)
+    got = out[torch.as_tensor(toks, device="cuda")].float().cpu().double().numpy()
+    assert O.rel_frobenius(got, ref) < 5e-3
