@@ -120,7 +120,12 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *                      2 = 512-wide (less L2 traffic, un-overlapped epilogue)
  *   "debug_mode"       overlap-ratio measurement: 0 normal, 1 computation only (no AG
  *                      copies or waits; results are garbage unless X_full already holds the data),
- *                      2 communication only (only the AG copy role runs)
+ *                      2 communication only (only the AG copy role runs), 3 (tests only) the AG-GEMM
+ *                      consumers skip their flag waits -- a deliberately broken protocol that the
+ *                      schedule-perturbation tests must catch
+ *   "debug_delay_ns"   (race detection) every producer notify, consumer wait and partial-tile push is
+ *                      preceded by a pseudo-random sleep of up to this many ns, keyed by (call, rank,
+ *                      tile) (default 0 = off); results must not change (tests/test_gpu_stress.py)
  *   "attn_poly"        tl_sp_attention: every n-th pair of exponentials is evaluated on the FMA pipe
  *                      (Cody-Waite + cubic) instead of MUFU (default 3; 0 = all on MUFU; 2,3,4,6,8) */
 tl_status tl_set_option(tl_comm_t comm, const char* key, int64_t value);

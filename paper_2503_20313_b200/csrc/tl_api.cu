@@ -142,7 +142,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3;
+          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0;
 };
 
 struct OptDesc {
@@ -164,8 +164,9 @@ const OptDesc kOpts[] = {
     {"n_sub", &Options::n_sub, 0, 2},
     {"ag_binding", &Options::ag_binding, 0, 1},
     {"dma_tile_rows", &Options::dma_tile_rows, 0, 1 << 20},
-    {"debug_mode", &Options::debug_mode, 0, 2},
+    {"debug_mode", &Options::debug_mode, 0, 3},
     {"attn_poly", &Options::attn_poly, 0, 8},
+    {"debug_delay_ns", &Options::debug_delay_ns, 0, 1000000},
 };
 
 }  // namespace
@@ -176,6 +177,7 @@ struct tl_comm {
   int64_t max_M = 0, max_H = 0;
   int max_topk = 1;
   unsigned moe_done = 0;            // CTA completions counted so far (identical on every rank)
+  uint32_t delay_calls = 0;         // seed of the debug schedule perturbation (debug_delay_ns)
   WsLayout lay{};
   uint8_t* ws[kMaxWorld] = {};      // workspace base of every rank (own, loopback-owned or IPC-mapped)
   bool owned[kMaxWorld] = {};       // cudaMalloc'd by us (else IPC-opened)
@@ -378,6 +380,8 @@ void fill_common(tl_comm* c, Params& p) {
   p.drop_rank = (int)c->opt.debug_drop_rank;
   p.drop_index = (int)c->opt.debug_drop_notify;
   p.debug_mode = (int)c->opt.debug_mode;
+  p.delay_ns = (uint32_t)c->opt.debug_delay_ns;
+  p.delay_seed = ++c->delay_calls;
 }
 
 // MoE first half (dynamic mapping): routing in, grouped tables out (per local rank).
@@ -1234,6 +1238,8 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
   p.diag = reinterpret_cast<Diag*>(c->ws[c->loopback ? 0 : c->rank] + c->lay.diag);
   p.drop_rank = (int)c->opt.debug_drop_rank;
   p.drop_index = (int)c->opt.debug_drop_notify;
+  p.delay_ns = (uint32_t)c->opt.debug_delay_ns;
+  p.delay_seed = ++c->delay_calls;
   p.tm_rows = sm.Tm;
   p.tiles_per_rank = sm.tiles_per_rank;
   p.tiles_per_channel = sm.tiles_per_channel;

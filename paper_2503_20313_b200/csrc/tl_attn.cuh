@@ -66,6 +66,7 @@ struct alignas(64) AttnParams {
   uint32_t epoch;
   int tm_rows, tiles_per_rank, tiles_per_channel, copy_ctas, row_bytes;
   int drop_rank, drop_index;
+  uint32_t delay_ns, delay_seed;   // schedule perturbation (debug_delay, 0 = off)
 };
 
 constexpr int kAttnThreads = 384;
@@ -335,7 +336,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
         }
         for (int j = 0; j < n_kv; ++j, ++g) {
           const int kvb = (j + rank * bpr) % n_kv;   // own shard first, then r+1, r+2, ...
-          if constexpr (kAG) attn_wait_rows(p, rank, kvb * 128, kvb * 128 + 128);
+          if constexpr (kAG) {
+            debug_delay(p.delay_ns, p.delay_seed, rank, 2 * j + 1);
+            attn_wait_rows(p, rank, kvb * 128, kvb * 128 + 128);
+          }
           const int st = g & 1;
           const uint32_t ph = (g >> 1) & 1;
           if (u == cta) TL_TRACE(4, j, 0);
@@ -433,6 +437,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
         const int n_tasks = p.tiles_per_rank * W;
         for (int task = cta; task < n_tasks; task += p.copy_ctas) {
           const int t = task / W, d = (rank + task % W) % W;
+          debug_delay(p.delay_ns, p.delay_seed, rank, 2 * task);
           const int lo = t * p.tm_rows, hi = min(lo + p.tm_rows, p.S_r);
           const uint32_t bytes = (uint32_t)(hi - lo) * (uint32_t)p.row_bytes;
           for (int kv = 0; kv < 2; ++kv) {

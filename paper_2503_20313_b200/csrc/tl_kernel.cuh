@@ -264,7 +264,10 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       const int row0 = mb * BM + cta_in_pair * 128;
       // dynamic mapping: this tile's rows are tokens [tok_lo, tok_hi] (sorted), gathered by id
       const int* tb = ra.moe_tab + 4 + 3 * mb;
-      if (kAG && p.debug_mode != 1) ag_wait_rows(p, rank, tb[1], tb[2] + 1);
+      if (kAG && p.debug_mode != 1) {
+        debug_delay(p.delay_ns, p.delay_seed, rank, 2 * item + 1);
+        ag_wait_rows(p, rank, tb[1], tb[2] + 1);
+      }
       const int4* src = reinterpret_cast<const int4*>(ra.moe_rows + row0) + g0;
 #pragma unroll
       for (int i = 0; i < kGPer; ++i) {
@@ -326,7 +329,10 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         else tile_coords(p, rank, ra.m_rot, t, mb, nb);
         const int row0 = mb * BM + cta_in_pair * 128;
         if constexpr (kAG) {
-          if (p.debug_mode != 1 && row0 < p.M) ag_wait_rows(p, rank, row0, min(row0 + 128, p.M));
+          if (p.debug_mode != 1 && row0 < p.M) {
+            debug_delay(p.delay_ns, p.delay_seed, rank, 2 * item + 1);
+            if (p.debug_mode != 3) ag_wait_rows(p, rank, row0, min(row0 + 128, p.M));
+          }
         }
         // the sub-tile count is a compile-time constant inside the k-loop (hoisted branch)
         auto produce = [&](auto ns_c, int s_lo) {
@@ -428,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         const int n_tasks = p.tiles_per_rank * W;
         for (int task = cta_in_rank; task < n_tasks; task += p.copy_ctas) {
           const int t = task / W, d = (rank + task % W) % W;  // tile-major, self first, then r+1, ...
+          debug_delay(p.delay_ns, p.delay_seed, rank, 2 * task);
           const int lo = t * p.tm_rows, hi = min(lo + p.tm_rows, p.M_r);
           const uint32_t bytes = (uint32_t)(hi - lo) * (uint32_t)p.row_bytes;
           const uint8_t* src = ra.a_shard + (size_t)lo * p.row_bytes;
@@ -528,6 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
             add_mask = ((1u << W) - 1) & ~(1u << rank);
           }
         }
+        debug_delay(p.delay_ns, p.delay_seed, rank * 4 + ew, 2 * item);
         if (push) {
           tm_out = &p.tm_stage[tgt];
           out_row = slot * p.M_r + lrow0 + ew * 32;
@@ -638,6 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       __threadfence_system();
       ptx::named_bar_sync(1, 128);
       if (ew == 0 && lane == 0) {
+        debug_delay(p.delay_ns, p.delay_seed, rank, cta_in_rank);
         const unsigned old = atomicAdd(ra.moe_done, 1u);
         if (old == p.moe_done_base + (unsigned)p.ctas_per_rank - 1u) {
           __threadfence_system();

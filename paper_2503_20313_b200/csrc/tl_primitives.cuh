@@ -92,6 +92,21 @@ __device__ __forceinline__ void tile_notify(uint32_t* flag, uint32_t epoch) {
   ptx::st_release_sys(flag, epoch);
 }
 
+// Race detection by schedule perturbation: a pseudo-random sleep of
+// up to max_ns ns keyed by (seed, a, b), placed before producer notifies, consumer waits and
+// partial-tile pushes.  A no-op unless the "debug_delay_ns" option is set; the stress tests then
+// require bit-identical results under many perturbed schedules.
+__device__ __forceinline__ void debug_delay(uint32_t max_ns, uint32_t seed, uint32_t a, uint32_t b) {
+  if (max_ns == 0) return;
+  uint32_t h = seed * 0x9E3779B1u ^ a * 0x85EBCA77u ^ b * 0xC2B2AE3Du;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  h *= 0x297A2D39u;
+  h ^= h >> 15;
+  __nanosleep(h % max_ns);
+}
+
 // consumer_tile_wait / peer_tile_wait: acquire, then order later async-proxy (TMA)
 // reads after it.
 __device__ __forceinline__ bool tile_wait(const uint32_t* flag, uint32_t epoch, uint64_t timeout_ns, Diag* diag,
