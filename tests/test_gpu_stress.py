@@ -172,3 +172,37 @@ def test_attention_bitwise_under_perturbed_schedules(tl, W):
         assert st == 0, diag
         for r in range(W):
             assert torch.equal(outs[r], ref[r]), f"delay {d} rank {r}"
+
+
+def test_thousand_back_to_back_calls_epoch_isolation(tl):
+    """SURVEY §4 test_epochs: 1000 back-to-back fused MLP calls over W = 4 loopback
+    ranks, alternating two input sets and interleaving standalone AG-GEMM / GEMM-RS calls (the AG and
+    RS epoch counters and banks cycle independently); every call is checked bit for bit against its
+    input set's first result."""
+    W, M, H, I = 4, 512, 256, 1024
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=H)
+    sets = []
+    for seed in (31, 32):
+        X, G, U, W2 = TI.mlp_full(M, H, I, seed=seed)
+        sets.append(tuple(_cuda(L) for L in TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)))
+    outs = [[torch.empty(M // W, H, device="cuda", dtype=torch.bfloat16) for _ in range(W)] for _ in range(2)]
+    Cs = [torch.empty(M, 2 * (I // W), device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    Ps = [torch.empty(M // W, H, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    Zs = [torch.zeros(M, I // W, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    got = []
+    for i in range(1000):                  # queued back to back: no host synchronisation in the loop
+        k = (i * 7 // 3) % 2
+        c.mlp_forward_lb(*sets[k], outs[k], act=TI.ACT_SILU_MUL)
+        got.append((k, torch.stack(outs[k]).clone()))
+        if i % 5 == 0:
+            c.ag_gemm_lb(sets[1 - k][0], sets[1 - k][1], Cs)     # an extra AG epoch
+        if i % 11 == 0:
+            c.gemm_rs_lb(Zs, sets[k][2], Ps)                      # an extra RS epoch
+    st, diag = c.check()
+    assert st == 0, diag
+    first = {}
+    for i, (k, o) in enumerate(got):
+        if k not in first:
+            first[k] = o
+        else:
+            assert torch.equal(o, first[k]), f"call {i}"
