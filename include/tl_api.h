@@ -126,6 +126,7 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *   "debug_delay_ns"   (race detection) every producer notify, consumer wait and partial-tile push is
  *                      preceded by a pseudo-random sleep of up to this many ns, keyed by (call, rank,
  *                      tile) (default 0 = off); results must not change (tests/test_gpu_stress.py)
+ *   "trace_events"     capacity of the device event trace (default 0 = off); see tl_trace_read
  *   "attn_poly"        tl_sp_attention: every n-th pair of exponentials is evaluated on the FMA pipe
  *                      (Cody-Waite + cubic) instead of MUFU (default 3; 0 = all on MUFU; 2,3,4,6,8) */
 tl_status tl_set_option(tl_comm_t comm, const char* key, int64_t value);
@@ -246,6 +247,17 @@ tl_status tl_sp_attention(tl_comm_t comm, const void* Q_shard, const void* K_sha
 tl_status tl_sp_attention_loopback(tl_comm_t comm, const void* const* Q_shard, const void* const* K_shard,
                                    const void* const* V_shard, void* const* O_shard, int64_t S, int heads,
                                    int head_dim, float scale, void* stream);
+
+/* ---------------------------------------------------------------- device event trace ------
+ * With option "trace_events" = N > 0 the fused GEMM kernels (AG-GEMM, GEMM-RS, MLP) append one
+ * 16-byte record per event to a comm-owned device buffer (SPEC S:418-421 TraceEvent):
+ *   struct { uint64 t_ns (%globaltimer); uint32 tile (bits 0-23; bits 24-31 = target rank of copy /
+ *            notify events); uint16 rank; uint8 unit (0 compute, 1 copy); uint8 kind (0 tile_start,
+ *            1 tile_end, 2 wait_start, 3 wait_end, 4 notify, 5 copy_start, 6 copy_end) }
+ * compute tile ids are the kernel's work-item index; copy / notify tile ids are AG producer tiles.
+ * tl_trace_read synchronises the device, copies min(recorded, cap) records to host memory `out`
+ * (cap * 16 bytes), sets *n_out, and empties the buffer.  No trace: *n_out = 0. */
+tl_status tl_trace_read(tl_comm_t comm, void* out, int64_t cap, int64_t* n_out);
 
 /* ---------------------------------------------------------------- diagnostics -------------
  * Evaluates the device-side static mapping for producer tiles t = 0..n-1 of a

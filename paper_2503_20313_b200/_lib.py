@@ -45,6 +45,7 @@ SIGNATURES = {
     "tl_moe_ag_gemm": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _int, _vp]),
     "tl_moe_ag_gemm_loopback": (_int, [_vp, _vpp, _vpp, _vpp, _vpp, _vpp, _vpp, _i64, _i64, _i64, _int, _int, _int,
                                        _vp]),
+    "tl_trace_read": (_int, [_vp, _vp, _i64, C.POINTER(_i64)]),
 }
 
 

@@ -142,7 +142,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0;
+          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0;
 };
 
 struct OptDesc {
@@ -167,6 +167,7 @@ const OptDesc kOpts[] = {
     {"debug_mode", &Options::debug_mode, 0, 3},
     {"attn_poly", &Options::attn_poly, 0, 8},
     {"debug_delay_ns", &Options::debug_delay_ns, 0, 1000000},
+    {"trace_events", &Options::trace_events, 0, 1ll << 28},
 };
 
 }  // namespace
@@ -178,6 +179,7 @@ struct tl_comm {
   int max_topk = 1;
   unsigned moe_done = 0;            // CTA completions counted so far (identical on every rank)
   uint32_t delay_calls = 0;         // seed of the debug schedule perturbation (debug_delay_ns)
+  TraceBuf* trace = nullptr;        // device event trace (option trace_events = capacity)
   WsLayout lay{};
   uint8_t* ws[kMaxWorld] = {};      // workspace base of every rank (own, loopback-owned or IPC-mapped)
   bool owned[kMaxWorld] = {};       // cudaMalloc'd by us (else IPC-opened)
@@ -382,6 +384,7 @@ void fill_common(tl_comm* c, Params& p) {
   p.debug_mode = (int)c->opt.debug_mode;
   p.delay_ns = (uint32_t)c->opt.debug_delay_ns;
   p.delay_seed = ++c->delay_calls;
+  p.trace = c->trace;
 }
 
 // MoE first half (dynamic mapping): routing in, grouped tables out (per local rank).
@@ -905,6 +908,7 @@ tl_status tl_comm_destroy(tl_comm_t c) {
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   for (int i = 0; i < kMaxWorld; ++i)
     if (c->moe_buf[i]) cudaFree(c->moe_buf[i]);
+  if (c->trace) cudaFree(c->trace);
   delete c;
   return TL_OK;
 }
@@ -924,10 +928,38 @@ tl_status tl_set_option(tl_comm_t c, const char* key, int64_t value) {
       if (value < d.lo || value > d.hi)
         return fail(TL_ERR_INVALID, "option %s=%lld outside [%lld, %lld]", key, (long long)value, (long long)d.lo,
                     (long long)d.hi);
+      if (!strcmp(key, "trace_events") && value != c->opt.trace_events) {   // (re)allocate the trace
+        TL_CUDA(cudaSetDevice(c->device));
+        TL_CUDA(cudaDeviceSynchronize());
+        if (c->trace) cudaFree(c->trace);
+        c->trace = nullptr;
+        if (value > 0) {
+          TL_CUDA(cudaMalloc(&c->trace, sizeof(TraceBuf) + (size_t)value * sizeof(TraceEv)));
+          const TraceBuf h = {0ull, (unsigned long long)value, {0ull, 0ull}};
+          TL_CUDA(cudaMemcpy(c->trace, &h, sizeof(h), cudaMemcpyHostToDevice));
+        }
+      }
       c->opt.*(d.field) = value;
       return TL_OK;
     }
   return fail(TL_ERR_INVALID, "unknown option '%s'", key);
+}
+
+tl_status tl_trace_read(tl_comm_t c, void* out, int64_t cap, int64_t* n_out) {
+  if (!c || !n_out || (cap > 0 && !out)) return fail(TL_ERR_INVALID, "null argument");
+  *n_out = 0;
+  if (!c->trace) return TL_OK;
+  TL_CUDA(cudaSetDevice(c->device));
+  TL_CUDA(cudaDeviceSynchronize());
+  TraceBuf h;
+  TL_CUDA(cudaMemcpy(&h, c->trace, sizeof(h), cudaMemcpyDeviceToHost));
+  const int64_t n = (int64_t)std::min<unsigned long long>(h.cursor, h.cap);
+  const int64_t m = std::min<int64_t>(n, cap);
+  if (m > 0) TL_CUDA(cudaMemcpy(out, c->trace + 1, (size_t)m * sizeof(TraceEv), cudaMemcpyDeviceToHost));
+  h.cursor = 0;
+  TL_CUDA(cudaMemcpy(c->trace, &h, sizeof(h), cudaMemcpyHostToDevice));
+  *n_out = m;   // == the capacity when the buffer filled up (later events were dropped)
+  return TL_OK;
 }
 
 tl_status tl_get_option(tl_comm_t c, const char* key, int64_t* value) {

@@ -331,7 +331,9 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         if constexpr (kAG) {
           if (p.debug_mode != 1 && row0 < p.M) {
             debug_delay(p.delay_ns, p.delay_seed, rank, 2 * item + 1);
+            if (cta_in_pair == 0) trace_ev(p.trace, TU_COMPUTE, TK_WAIT_START, rank, item);
             if (p.debug_mode != 3) ag_wait_rows(p, rank, row0, min(row0 + 128, p.M));
+            if (cta_in_pair == 0) trace_ev(p.trace, TU_COMPUTE, TK_WAIT_END, rank, item);
           }
         }
         // the sub-tile count is a compile-time constant inside the k-loop (hoisted branch)
@@ -395,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         const int as = it % kAccBufs;
         ptx::mbar_wait(&tempty[as], ((it / kAccBufs) & 1) ^ 1);
         ptx::tc_fence_after();
+        if (lane == 0) trace_ev(p.trace, TU_COMPUTE, TK_TILE_START, rank, item);
         const uint32_t tmem_d = tmem_base + as * kAccCols;
         auto issue = [&](auto ns_c, int s_lo) {
           constexpr int NS = decltype(ns_c)::value;
@@ -435,6 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         for (int task = cta_in_rank; task < n_tasks; task += p.copy_ctas) {
           const int t = task / W, d = (rank + task % W) % W;  // tile-major, self first, then r+1, ...
           debug_delay(p.delay_ns, p.delay_seed, rank, 2 * task);
+          trace_ev(p.trace, TU_COPY, TK_COPY_START, rank, t, d);
           const int lo = t * p.tm_rows, hi = min(lo + p.tm_rows, p.M_r);
           const uint32_t bytes = (uint32_t)(hi - lo) * (uint32_t)p.row_bytes;
           const uint8_t* src = ra.a_shard + (size_t)lo * p.row_bytes;
@@ -460,8 +464,10 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
           }
           g += n;
           ptx::bulk_wait<0>();  // every byte of this producer tile has landed at rank d
+          trace_ev(p.trace, TU_COPY, TK_COPY_END, rank, t, d);
           const bool drop = rank == p.drop_rank && t == p.drop_index && d == (rank + 1) % W;
           if (!drop) tile_notify(p.ag_flags[d] + rank * kAgFlagStride + t, p.epoch);
+          trace_ev(p.trace, TU_COPY, TK_NOTIFY, rank, t, d);
         }
       }
     }
@@ -500,6 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       if constexpr (kEpi == EPI_RS) {
         if (row0 >= p.M) {                                     // half-tile past the last row
           release_tmem();
+          if (cta_in_pair == 0 && ew == 0 && lane == 0) trace_ev(p.trace, TU_COMPUTE, TK_TILE_END, rank, item);
           continue;
         }
         const int W = p.world;
@@ -527,11 +534,13 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
           tgt = o;
           slot = rank;
           if (!push) {                                   // owner: peer_tile_wait on every other slot
+            if (cta_in_pair == 0 && ew == 0 && lane == 0) trace_ev(p.trace, TU_COMPUTE, TK_WAIT_START, rank, item);
             for (int q = 0; q < sub_n; ++q)
               if ((int)lane < W && (int)lane != rank)
                 tile_wait(p.rs_flags[rank] + lane * kRsFlagStride + tile + 4 * q, p.epoch, p.timeout_ns, p.diag,
                           rank, 2, lane, tile + 4 * q);
             __syncwarp();
+            if (cta_in_pair == 0 && ew == 0 && lane == 0) trace_ev(p.trace, TU_COMPUTE, TK_WAIT_END, rank, item);
             add_mask = ((1u << W) - 1) & ~(1u << rank);
           }
         }
@@ -633,9 +642,11 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         if (push && lane == 0) {
           ptx::bulk_wait<0>();
           for (int q = 0; q < sub_n; ++q) tile_notify(p.rs_flags[tgt] + slot * kRsFlagStride + tile + 4 * q, p.epoch);
+          if (cta_in_pair == 0 && ew == 0) trace_ev(p.trace, TU_COMPUTE, TK_NOTIFY, rank, item, tgt);
         }
         __syncwarp();
       }
+      if (cta_in_pair == 0 && ew == 0 && lane == 0) trace_ev(p.trace, TU_COMPUTE, TK_TILE_END, rank, item);
     }
     if (lane == 0) ptx::bulk_wait<0>();
     __syncwarp();

@@ -62,6 +62,7 @@ struct alignas(64) Params {
   // A read from whatever X_full holds), 2 = communication only (only the AG copy role runs)
   int debug_mode;
   uint32_t delay_ns, delay_seed;    // schedule perturbation (debug_delay, 0 = off)
+  TraceBuf* trace;                  // device event trace (null = off)
   int topk;           // MoE: routed slots per token
   unsigned int moe_done_base;       // MoE scatter: counter value before this call
   uint32_t* moe_flags[kMaxWorld];   // MoE scatter: [W slots] completion flags of rank o

@@ -92,6 +92,35 @@ __device__ __forceinline__ void tile_notify(uint32_t* flag, uint32_t epoch) {
   ptx::st_release_sys(flag, epoch);
 }
 
+// Device event trace (SURVEY §5 tracing; SPEC S:418-421 TraceEvent): 16-byte records appended
+// through an atomic cursor to a comm-owned buffer when the "trace_events" option is set (null
+// buffer = off: one uniform branch per event).  tile holds the tile id in bits 0-23 and, for copies
+// and notifies, the target rank in bits 24-31.
+struct TraceBuf {
+  unsigned long long cursor, cap, pad[2];   // header; records follow
+};
+struct TraceEv {
+  unsigned long long t_ns;
+  unsigned int tile;
+  unsigned short rank;
+  unsigned char unit, kind;
+};
+enum TraceUnit : int { TU_COMPUTE = 0, TU_COPY = 1 };
+enum TraceKind : int { TK_TILE_START = 0, TK_TILE_END = 1, TK_WAIT_START = 2, TK_WAIT_END = 3, TK_NOTIFY = 4,
+                       TK_COPY_START = 5, TK_COPY_END = 6 };
+__device__ __forceinline__ void trace_ev(TraceBuf* tb, int unit, int kind, int rank, int tile, int peer = 0) {
+  if (tb == nullptr) return;
+  const unsigned long long i = atomicAdd(&tb->cursor, 1ull);
+  if (i < tb->cap) {
+    TraceEv* ev = reinterpret_cast<TraceEv*>(tb + 1) + i;
+    ev->t_ns = ptx::globaltimer();
+    ev->tile = (unsigned)(tile & 0xFFFFFF) | ((unsigned)peer << 24);
+    ev->rank = (unsigned short)rank;
+    ev->unit = (unsigned char)unit;
+    ev->kind = (unsigned char)kind;
+  }
+}
+
 // Race detection by schedule perturbation: a pseudo-random sleep of
 // up to max_ns ns keyed by (seed, a, b), placed before producer notifies, consumer waits and
 // partial-tile pushes.  A no-op unless the "debug_delay_ns" option is set; the stress tests then
