@@ -416,6 +416,40 @@ def run_attention(args, helpers):
     b_total, _ = _timed(base_step, args.steps, args.warmup, barrier, stream, 2)
     bms = max_over_ranks(b_total) / args.steps
 
+    # overlap ratio of the fused AllGather-KV + attention (the paper's attention metric):
+    # W = 8 ranks emulated on this GPU; comp_only = the same launch without K/V traffic or waits,
+    # comm_only = only the copy role, overlap = the normal launch
+    loop = None
+    if not distributed:
+        LW = 8
+        lc = tl.Comm.loopback(LW, dev, S, 2 * h * D)
+        lQs, lKs, lVs = ([t.cuda() for t in L] for L in TI.attention_inputs(S, h, D, LW, seed=0))
+        lOs = [torch.empty_like(q) for q in lQs]
+
+        def lb_ms(mode, n=3):
+            lc.set_option("debug_mode", mode)
+            tl.sp_attention_lb(lc, lQs, lKs, lVs, lOs)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(n):
+                tl.sp_attention_lb(lc, lQs, lKs, lVs, lOs)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / n
+        loop = {"world": LW, "mode": "loopback (8 ranks on 1 GPU; K/V copies land in local HBM)"}
+        for binding, bname in ((0, "sm"), (1, "copy_engine")):
+            lc.set_option("ag_binding", binding)
+            ov, cp, cm = lb_ms(0), lb_ms(1), lb_ms(2)
+            lc.set_option("debug_mode", 0)
+            tl.sp_attention_lb(lc, lQs, lKs, lVs, lOs)
+            lst, _ = lc.check()
+            loop[f"ag_binding_{bname}"] = {
+                "overlap_ratio": {"comp_only_ms": round(cp, 4), "comm_only_ms": round(cm, 4),
+                                  "overlap_ms": round(ov, 4), "ratio": round((cp + cm - ov) / cm, 4)},
+                "tflops_whole_gpu": round(attn_flops(1) / (ov * 1e-3) / 1e12, 2), "status": int(lst)}
+        lc.close()
+
     cpu = None
     if rank == 0 and not distributed:
         rng = np.random.default_rng(1)
@@ -446,6 +480,7 @@ def run_attention(args, helpers):
         "gpu_launches": args.steps,
         "clocks": clk,
         "parity": parity,
+        "loopback_w8": loop,
         "baseline_torch": {"impl": "torch SDPA (cuDNN/flash backend as torch selects) (+ NCCL all_gather "
                                    "of K and V for W > 1)", "ms_per_step": round(bms, 4),
                            "value": round(fl * W / (bms * 1e-3) / 1e12, 2), "unit": "TFLOPS",

@@ -401,6 +401,58 @@ int64_t moe_capacity(int64_t M, int topk, int E, int BM) {
 }
 
 // ---------------------------------------------------------------- AG-GEMM (+ act)
+// Copy-engine AllGather (ag_binding = 1; rank_copy_data + rank_notify):
+// on a comm-owned stream per local rank, ordered after `stream`'s prior work, for every producer tile
+// t (tile-major) and destination d (self first) issue copy(i, r, d, lo, hi, copy_stream) for the
+// tile's rows [lo, hi), then write the epoch into d's flag of (r, t) with cuStreamWriteValue32
+// (system-wide fence before the write).  The kernel's consumer waits are the same as with SM copies.
+template <class CopyFn>
+tl_status dma_allgather(tl_comm* c, const StaticMap& sm, int64_t M_r, uint32_t epoch, cudaStream_t stream,
+                        CopyFn copy) {
+  const int W = c->world;
+  tl_status st = get_write_value();
+  if (st == TL_OK && !c->copy_stream[0]) {
+    cudaError_t e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
+    for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
+      e = cudaStreamCreateWithFlags(&c->copy_stream[i], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "copy stream setup: %s", cudaGetErrorString(e));
+  }
+  if (st != TL_OK) return st;
+  cudaError_t e = cudaEventRecord(c->ev_start, stream);
+  for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) e = cudaStreamWaitEvent(c->copy_stream[i], c->ev_start, 0);
+  for (int t = 0; e == cudaSuccess && t < sm.tiles_per_rank; ++t) {
+    const int64_t lo = (int64_t)t * sm.Tm, hi = std::min<int64_t>(lo + sm.Tm, M_r);
+    for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
+      const int r = local_rank_id(c, i);
+      for (int dd = 0; e == cudaSuccess && dd < W; ++dd) {
+        const int d = (r + dd) % W;
+        e = copy(i, r, d, lo, hi, c->copy_stream[i]);
+        if (e != cudaSuccess) break;
+        uint32_t* flag = reinterpret_cast<uint32_t*>(c->ws[d] + c->lay.ag_flags) + r * kAgFlagStride + t;
+        const bool drop = r == c->opt.debug_drop_rank && t == c->opt.debug_drop_notify && d == (r + 1) % W;
+        if (!drop && g_write_value(c->copy_stream[i], (CUdeviceptr)flag, epoch, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+                         CUDA_SUCCESS)
+          e = cudaErrorUnknown;
+      }
+    }
+  }
+  if (e != cudaSuccess) return fail(TL_ERR_CUDA, "copy-engine AllGather enqueue failed: %s", cudaGetErrorString(e));
+  return TL_OK;
+}
+
+// Join the copy streams back into `stream` (later work on it is ordered after every copy).
+tl_status dma_join(tl_comm* c, cudaStream_t stream) {
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
+    e = cudaEventRecord(c->ev_done[i], c->copy_stream[i]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, c->ev_done[i], 0);
+  }
+  if (e != cudaSuccess) return fail(TL_ERR_CUDA, "copy stream join: %s", cudaGetErrorString(e));
+  return TL_OK;
+}
+
 tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, void* const* C,
                        void* const* Agath, int64_t M, int64_t N_out, int64_t K, int act, cudaStream_t stream,
                        const MoeArgs* moe = nullptr) {
@@ -534,38 +586,11 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
     // rank_copy_data + rank_notify on the copy engines ("maps AllGather to the DMA
     // engine"): tile-major, self first; the GEMM kernel's consumer waits are unchanged.
     p.copy_ctas = 0;
-    st = get_write_value();
-    if (st == TL_OK && !c->copy_stream[0]) {
-      cudaError_t e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
-      for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
-        e = cudaStreamCreateWithFlags(&c->copy_stream[i], cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming);
-      }
-      if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "copy stream setup: %s", cudaGetErrorString(e));
-    }
-    if (st == TL_OK) {
-      cudaError_t e = cudaEventRecord(c->ev_start, stream);
-      for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) e = cudaStreamWaitEvent(c->copy_stream[i], c->ev_start, 0);
-      for (int t = 0; e == cudaSuccess && t < sm.tiles_per_rank; ++t) {
-        const int64_t lo = (int64_t)t * sm.Tm, hi = std::min<int64_t>(lo + sm.Tm, M_r);
-        for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
-          const int r = local_rank_id(c, i);
-          for (int dd = 0; e == cudaSuccess && dd < W; ++dd) {
-            const int d = (r + dd) % W;
-            uint8_t* dst = c->ws[d] + c->lay.xfull[bank] + ((size_t)r * M_r + lo) * K * 2;
-            e = cudaMemcpyAsync(dst, (const uint8_t*)A[i] + (size_t)lo * K * 2, (size_t)(hi - lo) * K * 2,
-                                cudaMemcpyDeviceToDevice, c->copy_stream[i]);
-            if (e != cudaSuccess) break;
-            uint32_t* flag = reinterpret_cast<uint32_t*>(c->ws[d] + c->lay.ag_flags) + r * kAgFlagStride + t;
-            const bool drop = r == c->opt.debug_drop_rank && t == c->opt.debug_drop_notify && d == (r + 1) % W;
-            if (!drop && g_write_value(c->copy_stream[i], (CUdeviceptr)flag, epoch, CU_STREAM_WRITE_VALUE_DEFAULT) !=
-                             CUDA_SUCCESS)
-              e = cudaErrorUnknown;
-          }
-        }
-      }
-      if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "copy-engine AllGather enqueue failed: %s", cudaGetErrorString(e));
-    }
+    st = dma_allgather(c, sm, M_r, epoch, stream, [&](int i, int r, int d, int64_t lo, int64_t hi, cudaStream_t cs) {
+      uint8_t* dst = c->ws[d] + c->lay.xfull[bank] + ((size_t)r * M_r + lo) * K * 2;
+      return cudaMemcpyAsync(dst, (const uint8_t*)A[i] + (size_t)lo * K * 2, (size_t)(hi - lo) * K * 2,
+                             cudaMemcpyDeviceToDevice, cs);
+    });
   }
   if (st == TL_OK && moe) {
     // dynamic mapping tables, built on the device from the routing, per local rank
@@ -607,14 +632,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
     const int epi = act == TL_ACT_NONE ? EPI_STORE : act == TL_ACT_SILU_MUL ? EPI_SILU_MUL : EPI_GELU_MUL;
     st = moe ? launch_moe(c, p, epi, comm, nsub, stream) : launch(c, p, epi, comm, nsub, stream);
   }
-  if (st == TL_OK && dma) {  // join: later work on `stream` is ordered after every copy
-    cudaError_t e = cudaSuccess;
-    for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
-      e = cudaEventRecord(c->ev_done[i], c->copy_stream[i]);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, c->ev_done[i], 0);
-    }
-    if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "copy stream join: %s", cudaGetErrorString(e));
-  }
+  if (st == TL_OK && dma) st = dma_join(c, stream);   // later work on `stream` follows every copy
   delete pp;
   if (st != TL_OK) return st;
   if (Agath) {
@@ -1244,7 +1262,12 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
   }
   if (S == 0 || heads == 0) return TL_OK;
   const int64_t row_bytes = row_elems * 2;
-  StaticMap sm = StaticMap::make((int)S, W, (int)std::max<int64_t>(1, std::min<int64_t>(c->opt.comm_tile_rows, S_r)),
+  // copy-engine binding: larger producer tiles (option dma_tile_rows, default S/world/4) so the host
+  // enqueues few large copies; SM binding: comm_tile_rows
+  const bool dma_bind = W > 1 && c->opt.ag_binding == 1;
+  const int64_t tm = dma_bind ? (c->opt.dma_tile_rows > 0 ? c->opt.dma_tile_rows : std::max<int64_t>(64, S_r / 4))
+                              : c->opt.comm_tile_rows;
+  StaticMap sm = StaticMap::make((int)S, W, (int)std::max<int64_t>(1, std::min<int64_t>(tm, S_r)),
                                  (int)c->opt.channels_per_rank);
   if (W > 1 && sm.tiles_per_rank > kAgFlagStride)
     return fail(TL_ERR_UNSUPPORTED, "too many producer tiles per rank (%d): raise comm_tile_rows", sm.tiles_per_rank);
@@ -1276,8 +1299,24 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
   p.tiles_per_rank = sm.tiles_per_rank;
   p.tiles_per_channel = sm.tiles_per_channel;
   p.copy_ctas = c->opt.copy_ctas > 0 ? (int)std::min<int64_t>(c->opt.copy_ctas, p.ctas_per_rank) : p.ctas_per_rank;
+  p.debug_mode = (c->opt.debug_mode == 1 || c->opt.debug_mode == 2) ? (int)c->opt.debug_mode : 0;
+  if (p.debug_mode == 1) p.copy_ctas = 0;   // computation only: no K/V AllGather traffic
   p.row_bytes = (int)row_bytes;
   const size_t kv_bytes = (size_t)S * row_bytes;
+  // ag_binding = 1: the K/V AllGather on the copy engines (the paper's binding for this workload,
+  // P:474 "uses host-side primitives ... copy engine"), leaving every SM to the attention
+  const bool dma = comm && c->opt.ag_binding == 1 && p.debug_mode != 1;
+  if (dma) {
+    p.copy_ctas = 0;
+    st = dma_allgather(c, sm, S_r, epoch, stream, [&](int i, int r, int d, int64_t lo, int64_t hi, cudaStream_t cs) {
+      uint8_t* kd = c->ws[d] + c->lay.xfull[bank] + ((size_t)r * S_r + lo) * row_bytes;
+      const size_t off = (size_t)lo * row_bytes, n = (size_t)(hi - lo) * row_bytes;
+      cudaError_t e = cudaMemcpyAsync(kd, (const uint8_t*)K[i] + off, n, cudaMemcpyDeviceToDevice, cs);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(kd + kv_bytes, (const uint8_t*)V[i] + off, n, cudaMemcpyDeviceToDevice, cs);
+      return e;
+    });
+  }
   if (comm)
     for (int d = 0; d < W; ++d) {
       p.kfull[d] = c->ws[d] + c->lay.xfull[bank];
@@ -1319,6 +1358,7 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
     }
     if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "attention launch: %s", cudaGetErrorString(e));
   }
+  if (st == TL_OK && dma) st = dma_join(c, stream);
   delete pp;
   return st;
 }

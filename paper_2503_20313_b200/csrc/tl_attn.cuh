@@ -67,6 +67,7 @@ struct alignas(64) AttnParams {
   int tm_rows, tiles_per_rank, tiles_per_channel, copy_ctas, row_bytes;
   int drop_rank, drop_index;
   uint32_t delay_ns, delay_seed;   // schedule perturbation (debug_delay, 0 = off)
+  int debug_mode;                  // overlap ratio: 1 computation only, 2 communication only
 };
 
 constexpr int kAttnThreads = 384;
@@ -95,6 +96,17 @@ __device__ __forceinline__ void attn_wait_rows(const AttnParams& p, int rank, in
     for (int t = c0 * p.tiles_per_channel; t < t_end; ++t)
       tile_wait(flags + s * kAgFlagStride + t, p.epoch, p.timeout_ns, p.diag, rank, 1, s, t);
   }
+}
+
+// KV block visited j-th by rank `rank` (W ranks, bpr blocks per shard, bpc blocks per round): round c
+// covers blocks [c bpc, (c+1) bpc) of every shard, own shard first, then r+1, ...  The AllGather
+// produces tile-major (tile t to every rank, then t+1), so a rank consumes the K/V blocks in about
+// the order they arrive rather than needing whole foreign shards early (W = 1: identity order).
+// Softmax is order-independent up to rounding; the order depends only on (W, rank, shard length).
+__device__ __forceinline__ int attn_kv_block(int j, int rank, int W, int bpr, int bpc) {
+  const int per_round = W * bpc;
+  const int c = j / per_round, rem = j - c * per_round;
+  return ((rank + rem / bpc) % W) * bpr + c * bpc + rem % bpc;
 }
 
 // ---- packed fp32x2 helpers (FFMA2 / FADD2 on sm_100) and the FMA-pipe exp2
@@ -273,8 +285,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
   const int cta = blockIdx.x % p.ctas_per_rank;
   const AttnRank& ra = p.rk[lr];
   const int rank = ra.rank;
-  const int nqb = p.S_r / 128, npairs = (nqb + 1) / 2, n_units = p.heads * npairs;
+  const int nqb = p.S_r / 128, npairs = (nqb + 1) / 2, n_units = p.debug_mode == 2 ? 0 : p.heads * npairs;
   const int n_kv = p.S / 128, bpr = p.S_r / 128;
+  // consumption order interleaves the shards block by block (see attn_kv_block); independent of the
+  // producer tile height, so the decoupled comm tile size never changes the result
+  const int bpc = 1;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::off_bar);
   uint64_t* q_full = bars + 0;    // [2] per tile
@@ -335,10 +350,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
           ptx::tma_load_3d<1>(&ra.tm_q, &q_full[x], q + 16384, 64, h, qb * 128);
         }
         for (int j = 0; j < n_kv; ++j, ++g) {
-          const int kvb = (j + rank * bpr) % n_kv;   // own shard first, then r+1, r+2, ...
+          const int kvb = attn_kv_block(j, rank, p.world, bpr, bpc);
           if constexpr (kAG) {
             debug_delay(p.delay_ns, p.delay_seed, rank, 2 * j + 1);
-            attn_wait_rows(p, rank, kvb * 128, kvb * 128 + 128);
+            if (p.debug_mode != 1) attn_wait_rows(p, rank, kvb * 128, kvb * 128 + 128);
           }
           const int st = g & 1;
           const uint32_t ph = (g >> 1) & 1;

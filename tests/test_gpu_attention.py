@@ -205,3 +205,35 @@ def test_attention_bench_config_w1_sampled(tl):
     ref = O.sp_attention([TI.to_f64(Qs[0])[rows]], [K64], [V64], D ** -0.5)[0]
     got = o[torch.as_tensor(rows, device="cuda")].float().cpu().double().numpy()
     assert O.rel_frobenius(got, ref) < TOL
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_attention_copy_engine_binding(tl, W):
+    """ag_binding = 1: the K/V AllGather runs on the copy engines (cudaMemcpyAsync per producer tile
+    and destination + stream write-value flags; the paper's binding for this workload) and the
+    kernel's waits are unchanged: bitwise equal to the SM binding over epoch-cycling calls, and
+    correct against the oracle."""
+    S, heads = 512 * W, 2
+    comm = _comm(tl, W, S, heads)
+    sm, ref = _run(tl, W, S, heads, comm=comm)
+    comm.set_option("ag_binding", 1)
+    dma, _ = _run(tl, W, S, heads, comm=comm, calls=3)
+    for call in dma:
+        for a, b in zip(call, sm[0]):
+            assert torch.equal(a, b)
+    assert _err(dma[-1], ref) < TOL
+
+
+def test_attention_copy_engine_dropped_notify_times_out(tl):
+    W, S, heads = 2, 512, 1
+    comm = _comm(tl, W, S, heads)
+    comm.set_option("ag_binding", 1)
+    comm.set_option("timeout_ms", 200)
+    comm.set_option("debug_drop_rank", 0)
+    comm.set_option("debug_drop_notify", 0)
+    Qs, Ks, Vs = TI.attention_inputs(S, heads, 128, W, seed=2)
+    qd, kd, vd = ([t.cuda() for t in L] for L in (Qs, Ks, Vs))
+    outs = [torch.empty_like(q) for q in qd]
+    tl.sp_attention_lb(comm, qd, kd, vd, outs)
+    st, diag = comm.check()
+    assert st != 0 and diag[1] == 1
