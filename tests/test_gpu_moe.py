@@ -32,6 +32,8 @@ def _run(tl, W, M, H, E, topk, N_out, act, skew=0.0, pair=2, placement=False, se
     comm = tl.Comm.loopback(W, 0, max_M=M, max_H=H) if W > 1 else tl.Comm.single(0, max_M=M, max_H=H)
     comm.set_option("cta_pair", pair)
     comm.set_option("n_sub", nsub)
+    for k, v in (options or {}).items():
+        comm.set_option(k, v)
     R = tl.moe_capacity(comm, M, topk, E)
     Ys = [torch.empty(R, N_out, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
     rows = [torch.empty(R, device="cuda", dtype=torch.int32) for _ in range(W)]
@@ -98,7 +100,8 @@ def test_moe_paper_shape_moe4_w8(tl):
 
 
 # ----------------------------------------------------------------------------- MoE second half + full layer
-def _moe_layer(tl, W, M, H, I, E, topk, act=TI.ACT_SILU_MUL, skew=0.0, calls=1, pair=2, nsub=0, seed=0):
+def _moe_layer(tl, W, M, H, I, E, topk, act=TI.ACT_SILU_MUL, skew=0.0, calls=1, pair=2, nsub=0, seed=0,
+               options=None):
     il = I // W
     X = TI._randn((M, H), seed, 0)
     Xs = TI.shard_rows(X, W)
@@ -110,6 +113,8 @@ def _moe_layer(tl, W, M, H, I, E, topk, act=TI.ACT_SILU_MUL, skew=0.0, calls=1, 
             else tl.Comm.single(0, max_M=M, max_H=H, max_topk=topk))
     comm.set_option("cta_pair", pair)
     comm.set_option("n_sub", nsub)
+    for k, v in (options or {}).items():
+        comm.set_option(k, v)
     R = tl.moe_capacity(comm, M, topk, E)
     Zg = [torch.empty(R, il, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
     rows = [torch.empty(R, device="cuda", dtype=torch.int32) for _ in range(W)]
@@ -154,6 +159,20 @@ def test_moe_layer_options_and_epochs(tl, pair, nsub):
     for later in results[1:]:
         for a, b in zip(later, results[0]):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_moe_layer_copy_engine_binding(tl, W):
+    """ag_binding = 1 (the paper's binding: AllGather on the copy engines) for the MoE first half:
+    bitwise equal to the SM-copy binding over epoch-cycling calls."""
+    kw = dict(M=256 * W, H=256, I=256 * W, E=8, topk=2, skew=0.5, calls=2)
+    sm_res, ref = _moe_layer(tl, W, **kw)
+    dma_res, _ = _moe_layer(tl, W, **kw, options={"ag_binding": 1})
+    for call in dma_res:
+        for a, b in zip(call, sm_res[0]):
+            assert torch.equal(a, b)
+    got = np.concatenate([o.float().cpu().double().numpy() for o in dma_res[-1]], 0)
+    assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
 
 
 def test_moe_layer_single_expert_matches_dense_mlp_kernels(tl):
