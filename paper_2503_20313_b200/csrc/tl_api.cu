@@ -1112,7 +1112,8 @@ tl_status moe_gemm_rs_impl(tl_comm* c, const void* const* Zg, const int32_t* con
     p.moe_flags[o] = reinterpret_cast<uint32_t*>(c->ws[o] + c->lay.moe_sync);
   }
   const int max_tiles = (int)(R_cap / BM);
-  const size_t need = (size_t)(4 + 3 * max_tiles + max_tiles + 4) * sizeof(int);
+  const size_t tab_ints = (size_t)(4 + 3 * max_tiles + max_tiles + 4);
+  const size_t need = ((tab_ints * sizeof(int) + 15) / 16) * 16 + (size_t)R_cap * sizeof(int4);
   for (int i = 0; st == TL_OK && i < c->n_local; ++i) {
     RankArgs& ra = p.rk[i];
     const int r = local_rank_id(c, i);
@@ -1127,7 +1128,10 @@ tl_status moe_gemm_rs_impl(tl_comm* c, const void* const* Zg, const int32_t* con
     }
     int* tab = c->moe_buf[i];
     int* sched = tab + 4 + 3 * max_tiles;
-    tl_moe_tiles_kernel<<<8, 256, 0, stream>>>(offs[i], E, BM, tab, sched);
+    int4* scat = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(tab) + ((tab_ints * sizeof(int) + 15) / 16) * 16);
+    tl_moe_tiles_kernel<<<32, 256, 0, stream>>>(offs[i], E, BM, tab, sched, rows[i], topk_w[i], topk, (int)M_r, r,
+                                                scat);
+    ra.moe_scat = scat;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { st = fail(TL_ERR_CUDA, "MoE tile table: %s", cudaGetErrorString(e)); break; }
     ra.moe_rows = rows[i];

@@ -116,6 +116,16 @@ __device__ __forceinline__ void moe_coords(const Params& p, const RankArgs& ra, 
   mt = ra.moe_sched[first + local % rows];
   expert = ra.moe_tab[4 + 3 * mt];
 }
+// The scatter flavour's schedule is the identity (tl_moe_tiles_kernel): its epilogue computes the
+// tile without loads (it needs no expert id).
+__device__ __forceinline__ int moe_scatter_tile(const Params& p, const RankArgs& ra, int item, int& nb) {
+  const int G = p.raster_group, n_tiles = ra.moe_tab[0];
+  const int per_group = G * p.n_blocks;
+  const int group = item / per_group, first = group * G;
+  const int rows = min(G, n_tiles - first), local = item - group * per_group;
+  nb = local / rows;
+  return first + local % rows;
+}
 
 // consumer_tile_wait for A rows [lo, hi) of the gathered tensor: every producer tile of every
 // channel those rows span must carry this call's epoch.
@@ -476,11 +486,15 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     const int ew = warp - 4;
     uint8_t* bufs = smem + L::off_epi + ew * 8192;
     int sbuf = 0, it = 0;
+    int pf_item = -1;                        // MoE scatter: item whose scatter target was prefetched
+    int4 pf_scat = make_int4(-1, 0, 0, 0);
     for (int item = pair; item < total; item += n_pairs, ++it) {
       int t, sub_lo, sub_n, mb, nb, expert;
       item_coords<kNSub>(p, item, t, sub_lo, sub_n);
-      if constexpr (kMoE) moe_coords(p, ra, item, mb, nb, expert);
+      if constexpr (kMoE == MOE_SCATTER) mb = moe_scatter_tile(p, ra, item, nb);
+      else if constexpr (kMoE) moe_coords(p, ra, item, mb, nb, expert);
       else tile_coords(p, rank, ra.m_rot, t, mb, nb);
+      (void)expert;
       const int as = it % kAccBufs;
       ptx::mbar_wait(&tfull[as], (it / kAccBufs) & 1);
       ptx::tc_fence_after();
@@ -552,16 +566,22 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
           out_row = lrow0 + ew * 32;
         }
       }
-      // MoE scatter: this thread's grouped row -> (token, slot), router weight, owner staging row
+      // MoE scatter: this thread's grouped row -> owner staging row and router weight (prefetched
+      // one item ahead: a single coalesced load whose latency overlaps the previous item's stores)
       uint16_t* moe_dst = nullptr;
       float moe_wt = 0.f;
       if constexpr (kEpi == EPI_MOE_SCATTER) {
-        const int rid = ra.moe_rows[row0 + ew * 32 + (int)lane];
-        if (rid >= 0) {
-          const int tok = rid / p.topk, kk = rid - tok * p.topk, o = tok / p.M_r;
-          moe_wt = ra.moe_w[rid];
-          moe_dst = const_cast<uint16_t*>(p.staging[o]) +
-                    (((size_t)rank * p.M_r + (tok - o * p.M_r)) * p.topk + kk) * (size_t)p.N_out;
+        const int4 sc = (item == pf_item) ? pf_scat : ra.moe_scat[row0 + ew * 32 + (int)lane];
+        if (sc.x >= 0) {
+          moe_wt = __int_as_float(sc.z);
+          moe_dst = const_cast<uint16_t*>(p.staging[sc.x]) + (size_t)sc.y * (size_t)p.N_out;
+        }
+        const int nxt = item + n_pairs;
+        if (nxt < total) {
+          int nb2;
+          const int mb2 = moe_scatter_tile(p, ra, nxt, nb2);
+          pf_item = nxt;
+          pf_scat = ra.moe_scat[mb2 * BM + cta_in_pair * 128 + ew * 32 + (int)lane];
         }
       }
       // piece -> 16 packed bf16x2 words (activation / slot reduction in fp32)
@@ -926,7 +946,8 @@ __global__ void __launch_bounds__(256) tl_moe_reduce_kernel(const __grid_constan
 
 // Tile table of a grouped layout from its padded group offsets (second MoE half): tab[0] = tiles,
 // tab[4 + 3 t] = expert of tile t; schedule = identity.
-__global__ void tl_moe_tiles_kernel(const int* offs, int E, int BM, int* tab, int* sched) {
+__global__ void tl_moe_tiles_kernel(const int* offs, int E, int BM, int* tab, int* sched, const int* rows,
+                                    const float* topk_w, int topk, int M_r, int rank, int4* scat) {
   const int n = offs[E] / BM;
   if (threadIdx.x == 0 && blockIdx.x == 0) tab[0] = n;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
@@ -936,6 +957,17 @@ __global__ void tl_moe_tiles_kernel(const int* offs, int E, int BM, int* tab, in
     tab[5 + 3 * t] = 0;
     tab[6 + 3 * t] = 0;
     sched[t] = t;
+  }
+  // scatter targets per grouped row, so the GEMM epilogue needs one coalesced load per row instead
+  // of the row id -> router weight chain: owner o = token / M_r, staging row (rank, token - o M_r, k)
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n * BM; g += gridDim.x * blockDim.x) {
+    const int rid = rows[g];
+    int4 v = make_int4(-1, 0, 0, 0);
+    if (rid >= 0) {
+      const int tok = rid / topk, k = rid - tok * topk, o = tok / M_r;
+      v = make_int4(o, (rank * M_r + (tok - o * M_r)) * topk + k, __float_as_int(topk_w[rid]), 0);
+    }
+    scat[g] = v;
   }
 }
 

@@ -35,6 +35,7 @@ struct alignas(64) RankArgs {
   const int* moe_tab;
   const int* moe_sched;
   const float* moe_w;         // MoE scatter: router weights [M, topk] (index = row id)
+  const int4* moe_scat;       // MoE scatter: per grouped row {owner, staging row, weight bits, -} (owner -1 = padding)
   unsigned int* moe_done;     // MoE scatter: this rank's CTA completion counter
 };
 

@@ -20,7 +20,7 @@ def tl():
     return m
 
 
-def _run(tl, W, M, H, E, topk, N_out, act, skew=0.0, pair=2, placement=False, seed=0, nsub=0):
+def _run(tl, W, M, H, E, topk, N_out, act, skew=0.0, pair=2, placement=False, seed=0, nsub=0, options=None):
     N1 = N_out * (1 if act == TI.ACT_NONE else 2)
     if placement:
         Xs, Ws = TI.moe_placement_inputs(M, H, E, N1, W)
