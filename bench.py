@@ -360,6 +360,9 @@ def main():
         base = {"impl": "nccl+cublas non-overlapped (torch.matmul, silu*mul, all_gather/reduce_scatter)",
                 "ms_per_step": round(bms, 4), "value": round((f1 + f2) * W / (bms * 1e-3) / 1e12, 2),
                 "unit": "TFLOPS", "speedup_ours": round(bms / ms, 4)}
+        if rank == 0:   # the baseline's own error against the same oracle rows
+            gb = ob.float().cpu().double().numpy()
+            base["parity_rel_fro"] = O.rel_frobenius(np.stack([gb[i] for i in rows]), np.stack([ref[i] for i in rows]))
 
     # ---- W = 8 ranks emulated on this GPU (full fused protocol, one launch per kernel)
     loop = None

@@ -84,6 +84,15 @@ def _timed(step, steps, warmup, barrier, stream, n_marks):
     return t0.elapsed_time(t1), seg
 
 
+def _traffic(key):
+    """DRAM bytes per launch of the dominant kernel from one committed ncu capture (profiles/traffic.json)."""
+    try:
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+        return json.load(open(path)).get(key)
+    except Exception:
+        return None
+
+
 def _common(metric, value, unit, W, args, ms, config):
     return {"metric": metric, "value": round(value, 2), "unit": unit, "n_gpus": W, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
@@ -283,7 +292,8 @@ def run_moe(args, helpers):
                      "achieved": round(ach1, 2), "peak": P_burst, "unit": "TFLOP/s", "frac": round(ach1 / P_burst, 4),
                      "frac_sustained": round(ach1 / P_sust, 4), "peak_source": peak_src,
                      "second_half": {"achieved": round(ach2, 2), "frac": round(ach2 / P_burst, 4)},
-                     "layer_frac": round(value / W / P_burst, 4), "traffic": None, "per_launch_flop": f1,
+                     "layer_frac": round(value / W / P_burst, 4), "traffic": _traffic("moe_ag_gemm_bytes") if W == 1 else None,
+                     "per_launch_flop": f1,
                      "flop_note": "routed rows only (S*topk); expert groups padded to 256 rows add ~6 % MMA work"},
         "cpu_baseline": cpu,
         "e2e": {"value": round((f1 + f2) * W / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
@@ -469,7 +479,8 @@ def run_attention(args, helpers):
         "kernels_ms": {"sp_attention": round(k1, 4)},
         "roofline": {"bound": "tensor", "kernel": "tl_attn_kernel (AG K/V + flash attention)",
                      "achieved": round(ach, 2), "peak": P_burst, "unit": "TFLOP/s", "frac": round(ach / P_burst, 4),
-                     "frac_sustained": round(ach / P_sust, 4), "peak_source": peak_src, "traffic": None,
+                     "frac_sustained": round(ach / P_sust, 4), "peak_source": peak_src,
+                     "traffic": _traffic("attention_bytes") if W == 1 else None,
                      "per_launch_flop": fl,
                      "note": "MUFU exp2 (16/clk/SM) co-limits: 128x128 scores per 2 x 128^3 MMA FLOPs"},
         "cpu_baseline": cpu,
