@@ -279,6 +279,27 @@ def run_moe(args, helpers):
     b_total, _ = _timed(base_step, args.steps, args.warmup, barrier, stream, 2)
     bms = max_over_ranks(b_total) / args.steps
 
+    # vLLM's fused MoE kernel (the paper's MoE baseline) on this rank's local problem
+    vllm = None
+    if not distributed:
+        try:
+            from vllm.model_executor.layers.fused_moe import fused_experts
+            xv = X.cuda()
+
+            def vllm_step(i, ev):
+                if ev:
+                    ev[0].record(stream)
+                fused_experts(xv, w1, w2, wts_d, ids_d)
+                if ev:
+                    ev[1].record(stream)
+            v_total, _ = _timed(vllm_step, args.steps, args.warmup, barrier, stream, 2)
+            vms = v_total / args.steps
+            vllm = {"impl": "vllm fused_experts (Triton fused MoE, both GEMMs + SiLU*up + weighted top-k sum)",
+                    "ms_per_step": round(vms, 4), "value": round((f1 + f2) / (vms * 1e-3) / 1e12, 2),
+                    "unit": "TFLOPS", "speedup_ours": round(vms / ms, 4)}
+        except Exception as e:   # baseline only: report why it could not run
+            vllm = {"unavailable": repr(e)[:200]}
+
     cpu = None
     if rank == 0 and not distributed:
         f = lambda L: [TI.to_f64(t) for t in L]
@@ -304,6 +325,7 @@ def run_moe(args, helpers):
         "gpu_launches": 5 * args.steps,
         "clocks": clk,
         "parity": parity,
+        "baseline_vllm": vllm,
         "baseline_torch": {"impl": "torch index_select + per-expert cuBLAS + silu*mul + per-expert cuBLAS + "
                                    "weighted index_add (+ NCCL all_gather / reduce_scatter for W > 1)",
                            "ms_per_step": round(bms, 4), "value": round((f1 + f2) * W / (bms * 1e-3) / 1e12, 2),
