@@ -70,3 +70,18 @@ def test_no_device_reports_cuda_error():
     st = L.tl_comm_create_loopback(2, 0, 256, 128, C.byref(h))
     assert st == _lib.TL_ERR_CUDA
     assert L.tl_last_error()
+
+
+def test_binding_rejects_host_and_mistyped_tensors_before_the_abi():
+    """The C ABI takes untyped pointers; the binding must refuse host memory, wrong dtypes,
+    non-contiguous views and inconsistent shapes before any pointer crosses it."""
+    import torch
+    import paper_2503_20313_b200 as tl
+    from paper_2503_20313_b200 import _check_mlp, _check_rs, _dev
+    x = torch.zeros(64, 128, dtype=torch.bfloat16)                         # host tensor
+    with pytest.raises(ValueError, match="CUDA"):
+        _check_mlp(2, 0, x, x, x, x, None, tl.ACT_SILU_MUL)
+    with pytest.raises(ValueError, match="CUDA"):
+        _check_rs(1, 0, torch.zeros(8, 8, dtype=torch.float32), x, x)
+    with pytest.raises(TypeError):
+        _dev([1, 2], "A", torch.bfloat16, (None,))

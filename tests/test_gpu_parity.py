@@ -495,3 +495,20 @@ def test_small_m_many_ranks(tl):
     ref = O.mlp_forward([TI.to_f64(x) for x in Xs], [TI.to_f64(w) for w in W1s], [TI.to_f64(w) for w in W2s],
                         TI.ACT_SILU_MUL)
     assert O.rel_frobenius(np.concatenate([f64(o) for o in outs], 0), np.concatenate(ref, 0)) < TOL
+
+
+def test_binding_shape_and_dtype_checks(tl):
+    """Shape / dtype / layout mistakes are caught in the binding (ValueError), not by a kernel."""
+    c = tl.Comm.single(0, max_M=512, max_H=256)
+    X, W1, W2 = empty(256, 128), empty(2 * 64, 128), empty(128, 64)
+    out = empty(256, 128)
+    c.mlp_forward(X, W1, W2, out, act=tl.ACT_SILU_MUL)                   # consistent: runs
+    assert c.check()[0] == 0
+    with pytest.raises(ValueError, match="shape"):
+        c.mlp_forward(X, empty(64, 128), W2, out, act=tl.ACT_SILU_MUL)     # W1 must be [2*I_l, H] gated
+    with pytest.raises(ValueError, match="bfloat16"):
+        c.mlp_forward(X.float(), W1, W2, out)
+    with pytest.raises(ValueError, match="contiguous"):
+        c.gemm_rs(empty(256, 128).t(), empty(64, 256), empty(128, 64))
+    with pytest.raises(ValueError, match="shape"):
+        c.ag_gemm(X, empty(64, 128), empty(256, 32))                      # B rows != C cols
