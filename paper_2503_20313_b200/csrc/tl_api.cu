@@ -194,6 +194,8 @@ struct tl_comm {
   // MoE tile tables per local rank (device): tab [4 + 3 * max_tiles] ints, sched [max_tiles], err
   int* moe_buf[kMaxWorld] = {};
   size_t moe_bytes[kMaxWorld] = {};
+  int* tab_sync[kMaxWorld] = {};            // routing-table kernel: per-CTA counts + grid-barrier counter
+  unsigned moe_tab_calls[kMaxWorld] = {};   // routing-table calls so far (2 barrier generations each)
 };
 
 namespace {
@@ -598,7 +600,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
     const int max_tiles = (int)(moe->R_cap / BM);
     p.topk = moe->topk;
     const size_t need = (size_t)(4 + 3 * max_tiles + max_tiles + 4) * sizeof(int);
-    const size_t smem = (size_t)(32 * moe->E + 2 * moe->E + 1 + max_tiles + kMoeThreads) * sizeof(int);
+    const size_t smem = (size_t)(kTabWarps * moe->E + 2 * moe->E + 1 + max_tiles + kTabThreads) * sizeof(int);
     // schedule key: expected-arrival bucket (W > 1) coarsened to <= 4 buckets, then expert
     int key_shift = 0;
     if (W == 1) key_shift = 30;
@@ -614,13 +616,22 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
         if (e != cudaSuccess) { st = fail(TL_ERR_CUDA, "MoE table alloc: %s", cudaGetErrorString(e)); break; }
         c->moe_bytes[i] = need;
       }
+      if (!c->tab_sync[i]) {   // [kTabCtas][1024] per-CTA expert counts + the grid-barrier counter
+        cudaError_t e = cudaMalloc(&c->tab_sync[i], ((size_t)kTabCtas * 1024 + 32) * sizeof(int));
+        if (e == cudaSuccess) e = cudaMemset(c->tab_sync[i], 0, ((size_t)kTabCtas * 1024 + 32) * sizeof(int));
+        if (e != cudaSuccess) { st = fail(TL_ERR_CUDA, "MoE table sync alloc: %s", cudaGetErrorString(e)); break; }
+        c->moe_tab_calls[i] = 0;
+      }
       int* tab = c->moe_buf[i];
       int* sched = tab + 4 + 3 * max_tiles;
       int* err = sched + max_tiles;
-      cudaFuncSetAttribute(tl_moe_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      tl_moe_tables_kernel<<<1, kMoeThreads, smem, stream>>>(moe->topk_ids[i], (int)(M * moe->topk), moe->topk,
-                                                             moe->E, BM, (int)M_r, sm.Tm, key_shift, moe->rows[i],
-                                                             moe->offs[i], tab, sched, max_tiles, err);
+      int* gcnt = c->tab_sync[i];
+      unsigned* gbar = reinterpret_cast<unsigned*>(gcnt + (size_t)kTabCtas * 1024);
+      const unsigned bar_base = c->moe_tab_calls[i]++ * 2u * kTabCtas;
+      cudaFuncSetAttribute(tl_moe_tables_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      tl_moe_tables_grid_kernel<<<kTabCtas, kTabThreads, smem, stream>>>(
+          moe->topk_ids[i], (int)(M * moe->topk), moe->topk, moe->E, BM, (int)M_r, sm.Tm, key_shift, moe->rows[i],
+          moe->offs[i], tab, sched, max_tiles, err, gcnt, gbar, bar_base);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) { st = fail(TL_ERR_CUDA, "MoE table kernel: %s", cudaGetErrorString(e)); break; }
       p.rk[i].moe_rows = moe->rows[i];
@@ -924,8 +935,10 @@ tl_status tl_comm_destroy(tl_comm_t c) {
     if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
   }
   if (c->ev_start) cudaEventDestroy(c->ev_start);
-  for (int i = 0; i < kMaxWorld; ++i)
+  for (int i = 0; i < kMaxWorld; ++i) {
     if (c->moe_buf[i]) cudaFree(c->moe_buf[i]);
+    if (c->tab_sync[i]) cudaFree(c->tab_sync[i]);
+  }
   if (c->trace) cudaFree(c->trace);
   delete c;
   return TL_OK;
@@ -1385,6 +1398,11 @@ tl_status tl_sp_attention_loopback(tl_comm_t c, const void* const* Q, const void
 
 }  // extern "C"
 
+#ifdef TL_TAB_TRACE
+extern "C" __attribute__((visibility("default"))) int tl_debug_tab_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, tl::g_tab_trace, sizeof(tl::g_tab_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 #ifdef TL_ATTN_TRACE
 extern "C" __attribute__((visibility("default"))) int tl_debug_attn_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, tl::g_attn_trace, sizeof(tl::g_attn_trace)) == cudaSuccess ? 0 : 1;

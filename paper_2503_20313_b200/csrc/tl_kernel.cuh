@@ -704,37 +704,6 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
 //   tab         {n_tiles, 0, 0, 0, then per tile: expert, first token, last token}  (f_S, f_R inputs),
 //   sched[j]    tiles ordered by the producer tile their last token lives in (expected arrival).
 // Every rank builds identical tables from the identical routing: no communication.
-constexpr int kMoeThreads = 1024;
-constexpr int kMoeLoadBatch = 16;   // routed entries in flight per lane (one memory latency per batch)
-
-// Exclusive scan of one int per thread over the 1024-thread block; *total = sum.  s32: 32 ints of
-// smem.  Called by every thread (contains block barriers).
-__device__ __forceinline__ int moe_block_scan(int v, int* s32, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s32[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int w = s32[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
-    }
-    s32[lane] = w;
-  }
-  __syncthreads();
-  const int base = warp ? s32[warp - 1] : 0;
-  *total = s32[31];
-  __syncthreads();   // s32 may be reused by the next call
-  return base + x - v;
-}
-
 // Lanes of the warp holding the same key (0 <= key < 2^nbits): nbits ballots.  Replaces
 // __match_any_sync, whose MATCH.ANY serialises (measured: the table kernel spent most of its 25 us
 // in 2 x 16 matches per warp).
@@ -746,126 +715,6 @@ __device__ __forceinline__ unsigned moe_peers(int key, int nbits) {
     m &= bit ? v : ~v;
   }
   return m;
-}
-
-// Dynamic tile-centric mapping tables from the routing, one CTA: stable counting sort of
-// the n = M * topk routed entries by expert (entry order inside an expert = (token, slot) order),
-// padded group offsets, per-tile {expert, first token, last token} and the tile schedule.
-// Every serial step of the first version (expert and bucket scans by one thread, one global-load
-// latency per 32 entries) is a block-wide scan or a batched load here.
-__global__ void __launch_bounds__(kMoeThreads, 1)
-    tl_moe_tables_kernel(const int* __restrict__ ids, int n, int topk, int E, int BM, int M_r, int Tm,
-                         int key_shift, int* rows, int* offs, int* tab, int* sched, int max_tiles, int* err) {
-  extern __shared__ int sh[];
-  int* wcnt = sh;                // [32 warps][E] per-warp counts, then per-warp running positions
-  int* cnt = wcnt + 32 * E;      // [E]
-  int* soffs = cnt + E;          // [E + 1]
-  int* keys = soffs + E + 1;     // [max_tiles]
-  int* bcnt = keys + max_tiles;  // [kMoeThreads] bucket counts -> starts
-  __shared__ int s32[32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // each warp owns one contiguous chunk of the routed entries (stable order = chunk order)
-  const int chunk = (n + 31) / 32, lo = warp * chunk, hi = min(lo + chunk, n);
-  const int nbits = 32 - __clz(E);   // keys e + 1 in [0, E]
-  for (int x = tid; x < 32 * E; x += kMoeThreads) wcnt[x] = 0;
-  __syncthreads();
-  for (int b0 = lo; b0 < hi; b0 += 32 * kMoeLoadBatch) {   // pass 1: per-warp expert histogram
-    int ev[kMoeLoadBatch];
-#pragma unroll
-    for (int u = 0; u < kMoeLoadBatch; ++u) {
-      const int i = b0 + u * 32 + lane;
-      ev[u] = i < hi ? __ldg(ids + i) : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < kMoeLoadBatch; ++u) {
-      const int i = b0 + u * 32 + lane;
-      int e = ev[u];
-      if (e >= E || (i < hi && e < 0)) {
-        atomicExch(err, 1);
-        e = -1;
-      }
-      if (e >= 0) atomicAdd(&wcnt[warp * E + e], 1);   // counts only: order is irrelevant here
-    }
-  }
-  __syncthreads();
-  // expert totals (parallel over experts), padded group offsets by a block scan (E <= 1024)
-  int my_cnt = 0;
-  if (tid < E) {
-    for (int w = 0; w < 32; ++w) my_cnt += wcnt[w * E + tid];
-    cnt[tid] = my_cnt;
-  }
-  int padded_total = 0;
-  const int my_off = moe_block_scan(tid < E ? (my_cnt + BM - 1) / BM * BM : 0, s32, &padded_total);
-  if (tid < E) {
-    soffs[tid] = my_off;
-    offs[tid] = my_off;
-    int run = my_off;                           // per-warp starting positions of this expert
-    for (int w = 0; w < 32; ++w) {
-      const int c = wcnt[w * E + tid];
-      wcnt[w * E + tid] = run;
-      run += c;
-    }
-    for (int g = my_off + my_cnt; g < my_off + (my_cnt + BM - 1) / BM * BM; ++g) rows[g] = -1;   // padding
-  }
-  if (tid == 0) {
-    soffs[E] = padded_total;
-    offs[E] = padded_total;
-    tab[0] = padded_total / BM;
-  }
-  __syncthreads();
-  for (int b0 = lo; b0 < hi; b0 += 32 * kMoeLoadBatch) {   // pass 2: place entries, stable per chunk
-    int ev[kMoeLoadBatch];
-#pragma unroll
-    for (int u = 0; u < kMoeLoadBatch; ++u) {
-      const int i = b0 + u * 32 + lane;
-      ev[u] = i < hi ? __ldg(ids + i) : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < kMoeLoadBatch; ++u) {
-      const int i = b0 + u * 32 + lane;
-      int e = ev[u];
-      if (e >= E) e = -1;
-      const unsigned peers = moe_peers(e + 1, nbits);   // lanes routing to the same expert
-      const int lrank = __popc(peers & ((1u << lane) - 1u));
-      if (e >= 0) rows[wcnt[warp * E + e] + lrank] = i;
-      __syncwarp();
-      if (e >= 0 && lrank == 0) wcnt[warp * E + e] += __popc(peers);
-      __syncwarp();
-    }
-  }
-  __syncthreads();   // rows[] written by other threads is read below (same CTA: bar.sync orders it)
-  const int n_tiles = padded_total / BM;
-  // tile table + schedule key: (producer tile of the tile's last token) >> key_shift, then expert,
-  // so tiles of one expert that become ready together run together (their B blocks shared in L2)
-  const int n_keys = ((M_r + Tm - 1) / Tm + (1 << key_shift) - 1) >> key_shift;
-  const int n_buckets = min(n_keys * E, kMoeThreads);
-  bcnt[tid] = 0;
-  __syncthreads();
-  for (int t = tid; t < n_tiles; t += kMoeThreads) {
-    const int g0 = t * BM;
-    int a = 0, b = E - 1;                       // expert e with soffs[e] <= g0 < soffs[e + 1]
-    while (a < b) {
-      const int mid = (a + b + 1) >> 1;
-      if (soffs[mid] <= g0) a = mid; else b = mid - 1;
-    }
-    const int e = a;
-    const int last = min(g0 + BM, soffs[e] + cnt[e]) - 1;
-    const int tlo = rows[g0] / topk, thi = rows[last] / topk;
-    tab[4 + 3 * t] = e;
-    tab[5 + 3 * t] = tlo;
-    tab[6 + 3 * t] = thi;
-    const int key = ((tlo / M_r == thi / M_r) ? (thi % M_r) / Tm : (M_r - 1) / Tm) >> key_shift;
-    keys[t] = min(key * E + e, n_buckets - 1);
-    atomicAdd(&bcnt[keys[t]], 1);
-  }
-  __syncthreads();
-  int n_sched = 0;
-  const int start = moe_block_scan(bcnt[tid], s32, &n_sched);
-  if (tid < n_buckets) {
-    int o = start;
-    for (int t = 0; t < n_tiles; ++t)
-      if (keys[t] == tid) sched[o++] = t;
-  }
 }
 
 // MoE owner reduction (TopK reduce + the reduce of ReduceScatter): once every source rank's slot
@@ -942,6 +791,232 @@ __global__ void __launch_bounds__(256) tl_moe_reduce_kernel(const __grid_constan
             make_uint4(ptx::pack_bf16x2(acc[v][0], acc[v][1]), ptx::pack_bf16x2(acc[v][2], acc[v][3]),
                        ptx::pack_bf16x2(acc[v][4], acc[v][5]), ptx::pack_bf16x2(acc[v][6], acc[v][7]));
   }
+}
+
+// ---- dynamic tile-centric mapping tables ("lookup tables, whose values can be filled at
+// runtime ... by other dynamic logics (e.g., dynamic routing)"), built on the device every call: a
+// stable counting sort of the M x topk routed entries by (expert, token), each expert's group padded
+// to the tile height, per tile {expert, first token, last token}, and a tile schedule ordered by the
+// producer tile each tile's last token lives in (expected AllGather arrival).  kTabCtas CTAs
+// (one per SM) that meet at two grid barriers (global arrival counter, monotone across calls: this
+// call's barriers complete at bar_base + G and bar_base + 2 G).  Phase 1: per-CTA, per-warp expert
+// histograms of contiguous entry chunks; phase 2: every CTA derives the padded group offsets and its
+// own starting position per expert (stable: chunk order = entry order) and places its entries;
+// phase 3 (CTA 0): per-tile table and schedule.
+constexpr int kTabCtas = 16, kTabThreads = 512, kTabWarps = kTabThreads / 32;
+constexpr int kTabBatch = 4;   // routed entries in flight per lane (chunks are small: n / 256 per warp)
+#ifdef TL_TAB_TRACE
+__device__ unsigned long long g_tab_trace[8];
+#define TAB_T(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_tab_trace[i] = ptx::globaltimer(); } while (0)
+#else
+#define TAB_T(i) do {} while (0)
+#endif
+
+__device__ __forceinline__ void tab_grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    const uint64_t t0 = ptx::globaltimer();
+    uint32_t n = 0;
+    while (ptx::ld_acquire_sys(bar) < target) {
+      __nanosleep(64);
+      if ((++n & 0x3FFu) == 0 && ptx::globaltimer() - t0 > 20000000000ull) __trap();   // never hang
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Exclusive scan of one int per thread over a 512-thread block (16 warps); *total = sum.
+__device__ __forceinline__ int tab_block_scan(int v, int* s32, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s32[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < kTabWarps ? s32[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    s32[lane] = w;
+  }
+  __syncthreads();
+  const int base = warp ? s32[warp - 1] : 0;
+  *total = s32[kTabWarps - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+__global__ void __launch_bounds__(kTabThreads, 1)
+    tl_moe_tables_grid_kernel(const int* __restrict__ ids, int n, int topk, int E, int BM, int M_r, int Tm,
+                              int key_shift, int* rows, int* offs, int* tab, int* sched, int max_tiles, int* err,
+                              int* gcnt, unsigned* gbar, unsigned bar_base) {
+  extern __shared__ int sh[];
+  int* wcnt = sh;                       // [16 warps][E]: counts, then running positions
+  int* cnt = wcnt + kTabWarps * E;      // [E] expert totals
+  int* soffs = cnt + E;                 // [E + 1] padded group offsets
+  int* keys = soffs + E + 1;            // [max_tiles] (CTA 0, phase 3)
+  int* bcnt = keys + max_tiles;         // [kTabThreads] bucket counts (CTA 0, phase 3)
+  __shared__ int s32[32];
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  TAB_T(0);
+  const int nbits = 32 - __clz(E);
+  const int cchunk = (n + G - 1) / G, clo = min(cta * cchunk, n), chi = min(clo + cchunk, n);
+  const int wchunk = (chi - clo + kTabWarps - 1) / kTabWarps;
+  const int lo = min(clo + warp * wchunk, chi), hi = min(lo + wchunk, chi);
+  for (int x = tid; x < kTabWarps * E; x += kTabThreads) wcnt[x] = 0;
+  __syncthreads();
+  for (int b0 = lo; b0 < hi; b0 += 32 * kTabBatch) {          // phase 1: per-warp histograms
+    int ev[kTabBatch];
+#pragma unroll
+    for (int u = 0; u < kTabBatch; ++u) {
+      const int i = b0 + u * 32 + lane;
+      ev[u] = i < hi ? __ldg(ids + i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kTabBatch; ++u) {
+      const int i = b0 + u * 32 + lane;
+      int e = ev[u];
+      if (e >= E || (i < hi && e < 0)) {
+        atomicExch(err, 1);
+        e = -1;
+      }
+      if (e >= 0) atomicAdd(&wcnt[warp * E + e], 1);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < E; e += kTabThreads) {   // this CTA's per-expert totals, per-warp prefixes
+    int run = 0;
+    for (int w = 0; w < kTabWarps; ++w) {
+      const int c = wcnt[w * E + e];
+      wcnt[w * E + e] = run;
+      run += c;
+    }
+    gcnt[cta * E + e] = run;
+  }
+  TAB_T(1);
+  tab_grid_barrier(gbar, bar_base + G);
+  TAB_T(2);
+  // phase 2: expert totals, padded offsets (block scan, 2 experts per thread: E <= 1024), and this
+  // CTA's start per expert = sum over the CTAs before it
+  int pc[2] = {0, 0}, mystart[2] = {0, 0}, pad_lo[2] = {0, 0}, pad_hi[2] = {0, 0};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int e = 2 * tid + k;
+    if (e < E) {
+      int v[kTabCtas], tot = 0, before = 0;
+#pragma unroll
+      for (int cc = 0; cc < kTabCtas; ++cc) v[cc] = cc < G ? __ldcg(gcnt + cc * E + e) : 0;   // all in flight
+#pragma unroll
+      for (int cc = 0; cc < kTabCtas; ++cc) {
+        tot += v[cc];
+        if (cc < cta) before += v[cc];
+      }
+      cnt[e] = tot;
+      pc[k] = (tot + BM - 1) / BM * BM;
+      mystart[k] = before;
+    }
+  }
+  int padded_total = 0;
+  TAB_T(5);
+  const int off0 = tab_block_scan(pc[0] + pc[1], s32, &padded_total);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int e = 2 * tid + k;
+    if (e < E) {
+      const int off = off0 + (k ? pc[0] : 0);
+      soffs[e] = off;
+      if (cta == 0) offs[e] = off;
+      for (int w = 0; w < kTabWarps; ++w) wcnt[w * E + e] += off + mystart[k];
+      if (e % G == cta) pad_lo[k] = off + cnt[e], pad_hi[k] = off + pc[k];
+    }
+  }
+  // padding rows (-1), spread over the warp of the owning thread's lane slots
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    unsigned todo = __ballot_sync(0xffffffffu, pad_hi[k] > pad_lo[k]);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int plo = __shfl_sync(0xffffffffu, pad_lo[k], src), phi = __shfl_sync(0xffffffffu, pad_hi[k], src);
+      for (int g = plo + lane; g < phi; g += 32) rows[g] = -1;
+    }
+  }
+  if (tid == 0) {
+    soffs[E] = padded_total;
+    if (cta == 0) {
+      offs[E] = padded_total;
+      tab[0] = padded_total / BM;
+    }
+  }
+  __syncthreads();
+  TAB_T(6);
+  for (int b0 = lo; b0 < hi; b0 += 32 * kTabBatch) {          // placement, stable per chunk
+    int ev[kTabBatch];
+#pragma unroll
+    for (int u = 0; u < kTabBatch; ++u) {
+      const int i = b0 + u * 32 + lane;
+      ev[u] = i < hi ? __ldg(ids + i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kTabBatch; ++u) {
+      const int i = b0 + u * 32 + lane;
+      int e = ev[u];
+      if (e >= E) e = -1;
+      const unsigned peers = moe_peers(e + 1, nbits);
+      const int lrank = __popc(peers & ((1u << lane) - 1u));
+      if (e >= 0) rows[wcnt[warp * E + e] + lrank] = i;
+      __syncwarp();
+      if (e >= 0 && lrank == 0) wcnt[warp * E + e] += __popc(peers);
+      __syncwarp();
+    }
+  }
+  TAB_T(3);
+  tab_grid_barrier(gbar, bar_base + 2 * G);
+  TAB_T(4);
+  if (cta != 0) return;
+  // phase 3 (CTA 0): tile table + schedule key (rows written by every CTA: read through L2)
+  const int n_tiles = padded_total / BM;
+  const int n_keys = ((M_r + Tm - 1) / Tm + (1 << key_shift) - 1) >> key_shift;
+  const int n_buckets = min(n_keys * E, kTabThreads);
+  bcnt[tid] = 0;
+  __syncthreads();
+  for (int t = tid; t < n_tiles; t += kTabThreads) {
+    const int g0 = t * BM;
+    int a = 0, b = E - 1;
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (soffs[mid] <= g0) a = mid; else b = mid - 1;
+    }
+    const int e = a;
+    const int last = min(g0 + BM, soffs[e] + cnt[e]) - 1;
+    const int tlo = __ldcg(rows + g0) / topk, thi = __ldcg(rows + last) / topk;
+    tab[4 + 3 * t] = e;
+    tab[5 + 3 * t] = tlo;
+    tab[6 + 3 * t] = thi;
+    const int key = ((tlo / M_r == thi / M_r) ? (thi % M_r) / Tm : (M_r - 1) / Tm) >> key_shift;
+    keys[t] = min(key * E + e, n_buckets - 1);
+    atomicAdd(&bcnt[keys[t]], 1);
+  }
+  __syncthreads();
+  int n_sched = 0;
+  const int start = tab_block_scan(bcnt[tid], s32, &n_sched);
+  if (tid < n_buckets) {
+    int o = start;
+    for (int t = 0; t < n_tiles; ++t)
+      if (keys[t] == tid) sched[o++] = t;
+  }
+  __syncthreads();
+  TAB_T(7);
 }
 
 // Tile table of a grouped layout from its padded group offsets (second MoE half): tab[0] = tiles,
