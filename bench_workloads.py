@@ -217,26 +217,25 @@ def run_moe(args, helpers):
         parity = {"tokens": len(toks), "rel_fro": O.rel_frobenius(got, ref), "tol": 5e-3, "status": int(st)}
 
     # e2e through the public API: X shard, routing and router weights in from pinned host memory,
-    # the layer, the output back to pinned host memory, every step (stream-ordered)
+    # the layer, the output back to pinned host memory, every step; the neighbouring steps' copies
+    # overlap the layer (pipeline.StepPipeline; the library calls stay ordered on one compute stream)
+    from paper_2503_20313_b200.pipeline import StepPipeline
     hx = x.cpu().pin_memory()
     hids, hwts = ids.pin_memory(), wts.pin_memory()
-    hout = torch.empty(Mr, H, dtype=torch.bfloat16).pin_memory()
-    xe, ide, wte = torch.empty_like(x), torch.empty_like(ids_d), torch.empty_like(wts_d)
+    hin = [[hx, hids, hwts] for _ in range(args.steps)]
+    hout = [[torch.empty(Mr, H, dtype=torch.bfloat16).pin_memory()] for _ in range(args.steps)]
 
-    def e2e_step(i, ev):
-        if ev:
-            ev[0].record(stream)
-        xe.copy_(hx, non_blocking=True)
-        ide.copy_(hids, non_blocking=True)
-        wte.copy_(hwts, non_blocking=True)
-        tl.moe_ag_gemm(comm, xe, ide, w1, Y, rows, offs, act=tl.ACT_SILU_MUL, stream=stream)
-        tl.moe_gemm_rs(comm, Y, rows, offs, wte, w2, out, stream=stream)
-        hout.copy_(out, non_blocking=True)
-        if ev:
-            ev[1].record(stream)
-    e2e_total, _ = _timed(e2e_step, args.steps, args.warmup, barrier, stream, 2)
-    e2e_ms = max_over_ranks(e2e_total) / args.steps
-    e2e_bytes_in = hx.numel() * 2 + hids.numel() * 4 + hwts.numel() * 4
+    def moe_fn(xin, xout, s):
+        tl.moe_ag_gemm(comm, xin[0], xin[1], w1, Y, rows, offs, act=tl.ACT_SILU_MUL, stream=s)
+        tl.moe_gemm_rs(comm, Y, rows, offs, xin[2], w2, xout[0], stream=s)
+    pipe = StepPipeline(moe_fn, [x, ids_d, wts_d], [out])
+    pipe.run(hin[:2], hout[:2])
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pipe.run(hin, hout, e0, e1)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    e2e_match = bool(torch.equal(hout[-1][0], out.cpu()))
 
     # library baseline: torch index gather + per-expert cuBLAS + silu*mul, per-expert cuBLAS + weighted
     # index_add (+ NCCL all_gather / reduce_scatter for W > 1), same inputs, same protocol
@@ -318,10 +317,10 @@ def run_moe(args, helpers):
                      "flop_note": "routed rows only (S*topk); expert groups padded to 256 rows add ~6 % MMA work"},
         "cpu_baseline": cpu,
         "e2e": {"value": round((f1 + f2) * W / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
-                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": e2e_bytes_in,
-                "d2h_bytes_per_step": hout.numel() * 2,
-                "api": "tl_moe_ag_gemm + tl_moe_gemm_rs (pinned host X shard, routing and router weights in, "
-                       "output back, every step, stream-ordered)"},
+                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": pipe.bytes_in,
+                "d2h_bytes_per_step": pipe.bytes_out, "output_matches_device_run": e2e_match,
+                "api": "tl_moe_ag_gemm + tl_moe_gemm_rs via pipeline.StepPipeline (pinned host X shard, routing "
+                       "and router weights in, output back, every step; neighbouring steps' copies overlap)"},
         "gpu_launches": 5 * args.steps,
         "clocks": clk,
         "parity": parity,
@@ -410,22 +409,19 @@ def run_attention(args, helpers):
         got = o[torch.as_tensor(rws, device="cuda")].float().cpu().double().numpy()
         parity = {"rows": len(rws), "rel_fro": O.rel_frobenius(got, ref), "tol": 5e-3, "status": int(st)}
 
+    from paper_2503_20313_b200.pipeline import StepPipeline
     hq, hk, hv = (t.pin_memory() for t in (Qs[rank], Ks[rank], Vs[rank]))
-    ho = torch.empty_like(hq).pin_memory()
-    qe, ke, ve = torch.empty_like(q), torch.empty_like(kk), torch.empty_like(v)
-
-    def e2e_step(i, ev):
-        if ev:
-            ev[0].record(stream)
-        qe.copy_(hq, non_blocking=True)
-        ke.copy_(hk, non_blocking=True)
-        ve.copy_(hv, non_blocking=True)
-        tl.sp_attention(comm, qe, ke, ve, o, stream=stream)
-        ho.copy_(o, non_blocking=True)
-        if ev:
-            ev[1].record(stream)
-    e2e_total, _ = _timed(e2e_step, args.steps, args.warmup, barrier, stream, 2)
-    e2e_ms = max_over_ranks(e2e_total) / args.steps
+    hin = [[hq, hk, hv] for _ in range(args.steps)]
+    hout = [[torch.empty_like(hq).pin_memory()] for _ in range(args.steps)]
+    pipe = StepPipeline(lambda xin, xout, s: tl.sp_attention(comm, xin[0], xin[1], xin[2], xout[0], stream=s),
+                        [q, kk, v], [o])
+    pipe.run(hin[:2], hout[:2])
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pipe.run(hin, hout, e0, e1)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    e2e_match = bool(torch.equal(hout[-1][0], o.cpu()))
 
     # library baseline: NCCL all_gather of K/V (W > 1) + torch SDPA (cuDNN / flash backends)
     kg = torch.empty(S, h, D, device="cuda", dtype=torch.bfloat16)
@@ -507,9 +503,10 @@ def run_attention(args, helpers):
                      "note": "MUFU exp2 (16/clk/SM) co-limits: 128x128 scores per 2 x 128^3 MMA FLOPs"},
         "cpu_baseline": cpu,
         "e2e": {"value": round(fl * W / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
-                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": 3 * hq.numel() * 2,
-                "d2h_bytes_per_step": ho.numel() * 2,
-                "api": "tl_sp_attention (pinned host Q/K/V shards in, O back, every step, stream-ordered)"},
+                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": pipe.bytes_in,
+                "d2h_bytes_per_step": pipe.bytes_out, "output_matches_device_run": e2e_match,
+                "api": "tl_sp_attention via pipeline.StepPipeline (pinned host Q/K/V shards in, O back, every "
+                       "step; neighbouring steps' copies overlap)"},
         "gpu_launches": args.steps,
         "clocks": clk,
         "parity": parity,
