@@ -127,6 +127,8 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *                      preceded by a pseudo-random sleep of up to this many ns, keyed by (call, rank,
  *                      tile) (default 0 = off); results must not change (tests/test_gpu_stress.py)
  *   "trace_events"     capacity of the device event trace (default 0 = off); see tl_trace_read
+ *   "pdl"              programmatic dependent launch of the GEMM kernels (default 1): their prologue
+ *                      may overlap the previous kernel in the stream (they wait before any data access)
  *   "attn_poly"        tl_sp_attention: every n-th pair of exponentials is evaluated on the FMA pipe
  *                      (Cody-Waite + cubic) instead of MUFU (default 3; 0 = all on MUFU; 2,3,4,6,8) */
 tl_status tl_set_option(tl_comm_t comm, const char* key, int64_t value);

@@ -142,7 +142,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0;
+          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1;
 };
 
 struct OptDesc {
@@ -168,6 +168,7 @@ const OptDesc kOpts[] = {
     {"attn_poly", &Options::attn_poly, 0, 8},
     {"debug_delay_ns", &Options::debug_delay_ns, 0, 1000000},
     {"trace_events", &Options::trace_events, 0, 1ll << 28},
+    {"pdl", &Options::pdl, 0, 1},
 };
 
 }  // namespace
@@ -260,13 +261,17 @@ tl_status launch_t(tl_comm* c, const Params& p, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = L::smem_request;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kPair;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // programmatic dependent launch (option "pdl", default on): the kernel's prologue may overlap the
+  // previous kernel in the stream; it executes griddepcontrol.wait before touching any data
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = c->opt.pdl ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   TL_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
   return TL_OK;
 }

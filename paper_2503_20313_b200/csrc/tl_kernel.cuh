@@ -223,8 +223,6 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
   const int pair = cta_in_rank / kPair, n_pairs = p.ctas_per_rank / kPair;
   const RankArgs& ra = p.rk[lr];
   const int rank = ra.rank;
-  // MoE: the number of m-tiles is data dependent (built on the device from the routing)
-  const int total = p.debug_mode == 2 ? 0 : kMoE ? ra.moe_tab[0] * p.n_blocks : p.n_items;
   constexpr int BM = 128 * kPair;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::off_bar);
@@ -258,6 +256,13 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
   if constexpr (kPair == 2) ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the prologue above (barrier init, TMEM allocation, descriptor
+  // prefetch) may overlap the previous kernel's tail; nothing it produced is touched before this wait.
+  // The next kernel may be scheduled onto SMs this grid releases (its own wait keeps it ordered).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // MoE: the number of m-tiles is data dependent (built on the device from the routing)
+  const int total = p.debug_mode == 2 ? 0 : kMoE ? ra.moe_tab[0] * p.n_blocks : p.n_items;
 
   // MoE producer: the 32 row gathers (tile::gather4) of every k-block are issued by two threads
   // (warp 0 lane 0: gathers 0-15 + the expert's B tile + the barrier arm; warp 2 lane 0: gathers
@@ -869,6 +874,7 @@ __global__ void __launch_bounds__(kTabThreads, 1)
   const int G = gridDim.x, cta = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TAB_T(0);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the GEMM's prologue may start
   const int nbits = 32 - __clz(E);
   const int cchunk = (n + G - 1) / G, clo = min(cta * cchunk, n), chi = min(clo + cchunk, n);
   const int wchunk = (chi - clo + kTabWarps - 1) / kTabWarps;
@@ -1023,6 +1029,7 @@ __global__ void __launch_bounds__(kTabThreads, 1)
 // tab[4 + 3 t] = expert of tile t; schedule = identity.
 __global__ void tl_moe_tiles_kernel(const int* offs, int E, int BM, int* tab, int* sched, const int* rows,
                                     const float* topk_w, int topk, int M_r, int rank, int4* scat) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the GEMM's prologue may start
   const int n = offs[E] / BM;
   if (threadIdx.x == 0 && blockIdx.x == 0) tab[0] = n;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
