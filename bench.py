@@ -473,4 +473,11 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    except Exception as exc:   # still emit one JSON line (rank 0) saying why the run could not complete
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": "TFLOPS",
+                              "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "error": repr(exc)[:400]}),
+                  flush=True)
+        raise
