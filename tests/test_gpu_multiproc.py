@@ -83,3 +83,98 @@ def test_two_processes_ipc_mlp():
         for o in outs:
             assert O.rel_frobenius(o.astype(np.float64), ref[r]) < 5e-3
         assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+def _worker_all(rank, world, port, q):
+    """One rank per process: the MLP layer, the MoE layer and SP attention through the
+    process-group comm (IPC-mapped peers), results sent back for the oracle check."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2503_20313_b200 as tl
+        import tl_inputs as TI
+        res = {}
+        # MLP
+        M, H, I = 128 * world, 128, 128 * world
+        X, G, U, W2 = TI.mlp_full(M, H, I, seed=6)
+        Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, world, TI.ACT_SILU_MUL)
+        comm = tl.Comm.from_process_group(None, 0, max_M=max(M, 512 * world), max_H=512, max_topk=2)
+        comm.set_option("num_ctas", max(2, 148 // world // 2 * 2))
+        comm.set_option("timeout_ms", 120000)
+        out = torch.empty(M // world, H, device="cuda", dtype=torch.bfloat16)
+        comm.mlp_forward(Xs[rank].cuda(), W1s[rank].cuda(), W2s[rank].cuda(), out, act=tl.ACT_SILU_MUL)
+        res["mlp"] = out.float().cpu().numpy()
+        # MoE (both halves)
+        E, topk, Hm, Im = 4, 2, 128, 128 * world
+        Xm = TI._randn((M, Hm), 7, 0)
+        W1m = TI.moe_weights(E, 2 * (Im // world), Hm, world, seed=8)
+        W2m = TI.moe_down_weights(E, Hm, Im // world, world, seed=9)
+        ids = TI.moe_routing(M, E, topk, seed=10)
+        wts = TI.moe_topk_weights(M, topk, seed=11)
+        R = tl.moe_capacity(comm, M, topk, E)
+        Y = torch.empty(R, Im // world, device="cuda", dtype=torch.bfloat16)
+        rows = torch.empty(R, device="cuda", dtype=torch.int32)
+        offs = torch.empty(E + 1, device="cuda", dtype=torch.int32)
+        mo = torch.empty(M // world, Hm, device="cuda", dtype=torch.bfloat16)
+        xm = TI.shard_rows(Xm, world)[rank].cuda()
+        tl.moe_ag_gemm(comm, xm, ids.cuda(), W1m[rank].cuda(), Y, rows, offs, act=tl.ACT_SILU_MUL)
+        tl.moe_gemm_rs(comm, Y, rows, offs, wts.cuda(), W2m[rank].cuda(), mo)
+        res["moe"] = mo.float().cpu().numpy()
+        # SP attention
+        S, heads = 256 * world, 2
+        Qs, Ks, Vs = TI.attention_inputs(S, heads, 128, world, seed=12)
+        ao = torch.empty(S // world, heads, 128, device="cuda", dtype=torch.bfloat16)
+        tl.sp_attention(comm, Qs[rank].cuda(), Ks[rank].cuda(), Vs[rank].cuda(), ao)
+        res["attn"] = ao.float().cpu().numpy()
+        st, diag = comm.check()
+        q.put((rank, st, res))
+        dist.barrier()
+        comm.close()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, "error", repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_processes_ipc_all_ops(world):
+    """Every fused op over real processes (one rank each, CUDA IPC peers; the GPU is time-shared)."""
+    import torch.multiprocessing as mp
+    import tl_inputs as TI
+    from oracle import tl_oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_all, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(world):
+        rank, st, res = q.get(timeout=900)
+        assert st != "error", res
+        assert st == 0
+        got[rank] = res
+    for p in procs:
+        p.join(timeout=120)
+    f = lambda L: [TI.to_f64(t) for t in L]
+    M, H, I = 128 * world, 128, 128 * world
+    X, G, U, W2 = TI.mlp_full(M, H, I, seed=6)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, world, TI.ACT_SILU_MUL)
+    ref = O.mlp_forward(f(Xs), f(W1s), f(W2s), TI.ACT_SILU_MUL)
+    E, topk, Hm, Im = 4, 2, 128, 128 * world
+    Xm = TI._randn((M, Hm), 7, 0)
+    W1m = TI.moe_weights(E, 2 * (Im // world), Hm, world, seed=8)
+    W2m = TI.moe_down_weights(E, Hm, Im // world, world, seed=9)
+    ids = TI.moe_routing(M, E, topk, seed=10)
+    wts = TI.moe_topk_weights(M, topk, seed=11)
+    ref_moe = O.moe_forward(f(TI.shard_rows(Xm, world)), ids.numpy(), wts.double().numpy(), f(W1m), f(W2m),
+                            TI.ACT_SILU_MUL)
+    S, heads = 256 * world, 2
+    Qs, Ks, Vs = TI.attention_inputs(S, heads, 128, world, seed=12)
+    ref_att = O.sp_attention(f(Qs), f(Ks), f(Vs), 128 ** -0.5)
+    for r in range(world):
+        assert O.rel_frobenius(got[r]["mlp"].astype(np.float64), ref[r]) < 5e-3
+        assert O.rel_frobenius(got[r]["moe"].astype(np.float64), ref_moe[r]) < 5e-3
+        assert O.rel_frobenius(got[r]["attn"].astype(np.float64), ref_att[r]) < 5e-3
