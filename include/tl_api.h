@@ -116,6 +116,13 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *   "ag_binding"       AllGather resource binding: 0 = SMs (bulk-copy warp in every CTA),
  *                      1 = copy engines (cudaMemcpyAsync + stream write-value flags)
  *   "dma_tile_rows"    producer-tile rows for ag_binding = 1 (default 0 = M/world/4, >= 64)
+ *   "rs_binding"       ReduceScatter resource binding: 0 = SMs (epilogue TMA-stores partial tiles into the
+ *                      owners' slots), 1 = the paper's hybrid: partial tiles to a local outbox,
+ *                      the copy engines move each finished chunk to its owner (stream wait on the
+ *                      kernel's chunk flag, cudaMemcpyAsync, stream write of the owner's flag), the
+ *                      owner reduces on SMs.  Not with rs_order = 1.
+ *   "rs_dma_rows"      rows per copy-engine chunk for rs_binding = 1 (default 0 = M/world; a multiple of
+ *                      128 dividing M/world)
  *   "n_sub"            256-column MMA sub-tiles per tile: 0 = auto, 1 = 256-wide (TMEM double-buffered),
  *                      2 = 512-wide (less L2 traffic, un-overlapped epilogue)
  *   "debug_mode"       overlap-ratio measurement: 0 normal, 1 computation only (no AG

@@ -94,6 +94,18 @@ tl_status get_write_value() {
   return TL_OK;
 }
 
+PFN_cuStreamWaitValue32_v11070 g_wait_value = nullptr;
+tl_status get_wait_value() {
+  if (g_wait_value) return TL_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || fn == nullptr || q != cudaDriverEntryPointSuccess)
+    return fail(TL_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable: copy-engine RS binding not supported");
+  g_wait_value = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fn);
+  return TL_OK;
+}
+
 tl_status get_encode() {
   if (g_encode) return TL_OK;
   void* fn = nullptr;
@@ -142,7 +154,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1;
+          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0;
 };
 
 struct OptDesc {
@@ -169,6 +181,8 @@ const OptDesc kOpts[] = {
     {"debug_delay_ns", &Options::debug_delay_ns, 0, 1000000},
     {"trace_events", &Options::trace_events, 0, 1ll << 28},
     {"pdl", &Options::pdl, 0, 1},
+    {"rs_binding", &Options::rs_binding, 0, 1},
+    {"rs_dma_rows", &Options::rs_dma_rows, 0, 1 << 20},
 };
 
 }  // namespace
@@ -195,7 +209,10 @@ struct tl_comm {
   // MoE tile tables per local rank (device): tab [4 + 3 * max_tiles] ints, sched [max_tiles], err
   int* moe_buf[kMaxWorld] = {};
   size_t moe_bytes[kMaxWorld] = {};
-  int* tab_sync[kMaxWorld] = {};            // routing-table kernel: per-CTA counts + grid-barrier counter
+  int* tab_sync[kMaxWorld] = {};
+  uint8_t* rs_outbox[kMaxWorld] = {};       // RS copy-engine binding: local outbox [world * M_r, N]
+  size_t rs_outbox_bytes[kMaxWorld] = {};
+  uint32_t* rs_dma_sync[kMaxWorld] = {};    // [2][world][kRsFlagStride]: chunk counters, ready flags            // routing-table kernel: per-CTA counts + grid-barrier counter
   unsigned moe_tab_calls[kMaxWorld] = {};   // routing-table calls so far (2 barrier generations each)
 };
 
@@ -413,19 +430,24 @@ int64_t moe_capacity(int64_t M, int topk, int E, int BM) {
 // t (tile-major) and destination d (self first) issue copy(i, r, d, lo, hi, copy_stream) for the
 // tile's rows [lo, hi), then write the epoch into d's flag of (r, t) with cuStreamWriteValue32
 // (system-wide fence before the write).  The kernel's consumer waits are the same as with SM copies.
+// One comm-owned copy stream (+ completion event) per local rank, created on first use.
+tl_status dma_streams(tl_comm* c) {
+  if (c->copy_stream[0]) return TL_OK;
+  cudaError_t e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
+  for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
+    e = cudaStreamCreateWithFlags(&c->copy_stream[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) return fail(TL_ERR_CUDA, "copy stream setup: %s", cudaGetErrorString(e));
+  return TL_OK;
+}
+
 template <class CopyFn>
 tl_status dma_allgather(tl_comm* c, const StaticMap& sm, int64_t M_r, uint32_t epoch, cudaStream_t stream,
                         CopyFn copy) {
   const int W = c->world;
   tl_status st = get_write_value();
-  if (st == TL_OK && !c->copy_stream[0]) {
-    cudaError_t e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
-    for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
-      e = cudaStreamCreateWithFlags(&c->copy_stream[i], cudaStreamNonBlocking);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming);
-    }
-    if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "copy stream setup: %s", cudaGetErrorString(e));
-  }
+  if (st == TL_OK) st = dma_streams(c);
   if (st != TL_OK) return st;
   cudaError_t e = cudaEventRecord(c->ev_start, stream);
   for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) e = cudaStreamWaitEvent(c->copy_stream[i], c->ev_start, 0);
@@ -713,11 +735,23 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
   p.n_blocks = (int)n_blocks;
   p.k_blocks = (int)((K + kBK - 1) / kBK);
   set_items(p, nsub, p.ctas_per_rank / pair);
-  p.rs_mode = comm ? (c->opt.rs_order == 1 ? RS_RING : RS_ONESHOT) : RS_NONE;
+  const bool dma = comm && c->opt.rs_binding == 1;
+  p.rs_mode = comm ? (dma ? RS_DMA : c->opt.rs_order == 1 ? RS_RING : RS_ONESHOT) : RS_NONE;
   p.order = comm ? ORDER_ROTATE : ORDER_IDENTITY;
   p.tm_rows = 1;
   p.tiles_per_rank = 1;
   p.tiles_per_channel = 1;
+  const int64_t chunk = dma ? (c->opt.rs_dma_rows > 0 ? c->opt.rs_dma_rows : M_r) : 128;
+  if (dma) {
+    if (c->opt.rs_order == 1) st = fail(TL_ERR_UNSUPPORTED, "rs_binding = 1 (copy engines) has no ring order");
+    else if (chunk % 128 || M_r % chunk)
+      st = fail(TL_ERR_UNSUPPORTED, "rs_dma_rows=%lld must be a multiple of 128 dividing M/world=%lld",
+                (long long)chunk, (long long)M_r);
+    else if (st == TL_OK) st = get_wait_value();
+    if (st == TL_OK) st = get_write_value();
+    p.rs_chunk_rows = (int)chunk;
+    p.rs_cnt_target = (unsigned)((chunk / 128) * 4 * n_blocks * nsub);
+  }
   if (comm) {
     for (int o = 0; o < W; ++o) {
       uint8_t* sb = c->ws[o] + c->lay.stage[bank];
@@ -735,8 +769,70 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
     if ((st = cached_tmap(c, &ra.tm_a, A[i], M, K, 128, 64)) != TL_OK) break;
     if ((st = cached_tmap(c, &ra.tm_b0, B[i], N, K, pair == 2 ? 128 : 256, 64)) != TL_OK) break;
     if ((st = cached_tmap(c, &ra.tm_c, C[i], comm ? M_r : M, N, 32, 64)) != TL_OK) break;
+    if (dma) {   // local outbox + chunk counters / ready flags of this rank
+      const size_t ob = (size_t)W * M_r * N * 2;
+      if (c->rs_outbox_bytes[i] < ob) {
+        if (c->rs_outbox[i]) {
+          TL_CUDA(cudaStreamSynchronize(stream));
+          cudaFree(c->rs_outbox[i]);
+        }
+        c->rs_outbox[i] = nullptr;
+        c->rs_outbox_bytes[i] = 0;
+        TL_CUDA(cudaMalloc(&c->rs_outbox[i], ob));
+        c->rs_outbox_bytes[i] = ob;
+      }
+      if (!c->rs_dma_sync[i]) {
+        const size_t sb = (size_t)2 * kMaxWorld * kRsFlagStride * sizeof(uint32_t);
+        TL_CUDA(cudaMalloc(&c->rs_dma_sync[i], sb));
+        TL_CUDA(cudaMemset(c->rs_dma_sync[i], 0, sb));
+      }
+      p.rs_cnt[i] = c->rs_dma_sync[i];
+      p.rs_ready[i] = c->rs_dma_sync[i] + (size_t)kMaxWorld * kRsFlagStride;
+      if ((st = cached_tmap(c, &p.tm_outbox[i], c->rs_outbox[i], (uint64_t)W * M_r, N, 32, 64)) != TL_OK) break;
+    }
+  }
+  // The kernel is enqueued before the copy streams' waits: streams can share hardware queues
+  // (CUDA_DEVICE_MAX_CONNECTIONS), and a wait-value queued ahead of the kernel that satisfies it would
+  // deadlock.  The copy streams are ordered after the work that precedes the kernel (ev_start), never
+  // after the kernel itself.
+  if (st == TL_OK && dma) {
+    st = dma_streams(c);
+    if (st == TL_OK && cudaEventRecord(c->ev_start, stream) != cudaSuccess) st = fail(TL_ERR_CUDA, "event record");
   }
   if (st == TL_OK) st = launch(c, p, comm ? EPI_RS : EPI_STORE, false, nsub, stream);
+  if (st == TL_OK && dma) {
+    // rank_copy_data + rank_notify for the scatter: per local rank, in the kernel's owner order,
+    // for every chunk: wait for the kernel's ready flag, copy the chunk from the outbox into the owner's
+    // staging slot, write the epoch into the owner's flag of (slot, chunk)
+    {
+      cudaError_t e = cudaSuccess;
+      for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) e = cudaStreamWaitEvent(c->copy_stream[i], c->ev_start, 0);
+      const int64_t n_chunks = M_r / chunk;
+      for (int i = 0; e == cudaSuccess && i < c->n_local; ++i) {
+        const int r = local_rank_id(c, i);
+        for (int oo = 1; e == cudaSuccess && oo < W; ++oo) {
+          const int o = (r + oo) % W;
+          for (int64_t b = 0; e == cudaSuccess && b < n_chunks; ++b) {
+            uint32_t* ready = p.rs_ready[i] + (size_t)o * kRsFlagStride + b;
+            if (g_wait_value(c->copy_stream[i], (CUdeviceptr)ready, epoch, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+              e = cudaErrorUnknown;
+              break;
+            }
+            const size_t bytes = (size_t)chunk * N * 2;
+            uint8_t* dst = c->ws[o] + c->lay.stage[bank] + ((size_t)r * M_r + b * chunk) * N * 2;
+            const uint8_t* src = c->rs_outbox[i] + ((size_t)o * M_r + b * chunk) * N * 2;
+            e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->copy_stream[i]);
+            if (e != cudaSuccess) break;
+            uint32_t* flag = reinterpret_cast<uint32_t*>(c->ws[o] + c->lay.rs_flags) + (size_t)r * kRsFlagStride + b;
+            if (g_write_value(c->copy_stream[i], (CUdeviceptr)flag, epoch, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+              e = cudaErrorUnknown;
+          }
+        }
+      }
+      if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "copy-engine scatter enqueue failed: %s", cudaGetErrorString(e));
+    }
+  }
+  if (st == TL_OK && dma) st = dma_join(c, stream);
   delete pp;
   return st;
 }
@@ -943,6 +1039,8 @@ tl_status tl_comm_destroy(tl_comm_t c) {
   for (int i = 0; i < kMaxWorld; ++i) {
     if (c->moe_buf[i]) cudaFree(c->moe_buf[i]);
     if (c->tab_sync[i]) cudaFree(c->tab_sync[i]);
+    if (c->rs_outbox[i]) cudaFree(c->rs_outbox[i]);
+    if (c->rs_dma_sync[i]) cudaFree(c->rs_dma_sync[i]);
   }
   if (c->trace) cudaFree(c->trace);
   delete c;

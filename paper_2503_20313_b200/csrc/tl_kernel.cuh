@@ -554,17 +554,26 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
           slot = rank;
           if (!push) {                                   // owner: peer_tile_wait on every other slot
             if (cta_in_pair == 0 && ew == 0 && lane == 0) trace_ev(p.trace, TU_COMPUTE, TK_WAIT_START, rank, item);
-            for (int q = 0; q < sub_n; ++q)
+            if (p.rs_mode == RS_DMA) {                   // one flag per (slot, chunk), set by the copy engine
               if ((int)lane < W && (int)lane != rank)
-                tile_wait(p.rs_flags[rank] + lane * kRsFlagStride + tile + 4 * q, p.epoch, p.timeout_ns, p.diag,
-                          rank, 2, lane, tile + 4 * q);
+                tile_wait(p.rs_flags[rank] + lane * kRsFlagStride + lrow0 / p.rs_chunk_rows, p.epoch, p.timeout_ns,
+                          p.diag, rank, 2, lane, lrow0 / p.rs_chunk_rows);
+            } else {
+              for (int q = 0; q < sub_n; ++q)
+                if ((int)lane < W && (int)lane != rank)
+                  tile_wait(p.rs_flags[rank] + lane * kRsFlagStride + tile + 4 * q, p.epoch, p.timeout_ns, p.diag,
+                            rank, 2, lane, tile + 4 * q);
+            }
             __syncwarp();
             if (cta_in_pair == 0 && ew == 0 && lane == 0) trace_ev(p.trace, TU_COMPUTE, TK_WAIT_END, rank, item);
             add_mask = ((1u << W) - 1) & ~(1u << rank);
           }
         }
         debug_delay(p.delay_ns, p.delay_seed, rank * 4 + ew, 2 * item);
-        if (push) {
+        if (push && p.rs_mode == RS_DMA) {               // to the local outbox, block of owner o
+          tm_out = &p.tm_outbox[lr];
+          out_row = o * p.M_r + lrow0 + ew * 32;
+        } else if (push) {
           tm_out = &p.tm_stage[tgt];
           out_row = slot * p.M_r + lrow0 + ew * 32;
         } else {
@@ -666,7 +675,22 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         // buffer was already released, so the wait overlaps the next tile's MMAs.
         if (push && lane == 0) {
           ptx::bulk_wait<0>();
-          for (int q = 0; q < sub_n; ++q) tile_notify(p.rs_flags[tgt] + slot * kRsFlagStride + tile + 4 * q, p.epoch);
+          if (p.rs_mode == RS_DMA) {
+            // count this warp slice into its (owner, chunk); the last one resets the counter for the
+            // next call and releases the chunk to the copy engine (epoch-valued flag)
+            const int blk = (row0 - tgt * p.M_r) / p.rs_chunk_rows;
+            ptx::fence_proxy_async_global();
+            __threadfence();
+            unsigned* cnt = p.rs_cnt[lr] + tgt * kRsFlagStride + blk;
+            const unsigned old = atomicAdd(cnt, (unsigned)sub_n);
+            if (old + (unsigned)sub_n == p.rs_cnt_target) {
+              atomicExch(cnt, 0u);
+              __threadfence_system();
+              ptx::st_release_sys(p.rs_ready[lr] + tgt * kRsFlagStride + blk, p.epoch);
+            }
+          } else {
+            for (int q = 0; q < sub_n; ++q) tile_notify(p.rs_flags[tgt] + slot * kRsFlagStride + tile + 4 * q, p.epoch);
+          }
           if (cta_in_pair == 0 && ew == 0) trace_ev(p.trace, TU_COMPUTE, TK_NOTIFY, rank, item, tgt);
         }
         __syncwarp();
@@ -675,6 +699,15 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     }
     if (lane == 0) ptx::bulk_wait<0>();
     __syncwarp();
+    if constexpr (kEpi == EPI_RS) {
+      // RS_DMA fail-safe: the host-enqueued copy streams wait on this rank's chunk flags with no
+      // timeout; after a device-side timeout (diag set) release them all so they drain instead of
+      // hanging the process (the call still reports TL_ERR_TIMEOUT through tl_comm_check)
+      if (p.rs_mode == RS_DMA && ew == 0 && lane == 0 &&
+          *reinterpret_cast<volatile unsigned long long*>(&p.diag->status) != 0ull)
+        for (int o = 0; o < p.world; ++o)
+          for (int b = 0; b < p.M_r / p.rs_chunk_rows; ++b) ptx::st_release_sys(p.rs_ready[lr] + o * kRsFlagStride + b, p.epoch);
+    }
     if constexpr (kEpi == EPI_MOE_SCATTER) {
       // every CTA of this rank counts itself done; the last one releases this rank's slot flag on
       // every owner (peer_tile_notify at whole-operator granularity: the scatter targets are data

@@ -18,7 +18,11 @@ enum Epi : int { EPI_STORE = 0, EPI_SILU_MUL = 1, EPI_GELU_MUL = 2, EPI_RS = 3, 
 // whose epilogue scatters weighted rows to the owners' staging slots (GroupGEMM + Scatter + TopK + RS)
 enum MoeKind : int { MOE_NONE = 0, MOE_GATHER = 1, MOE_SCATTER = 2 };
 enum Order : int { ORDER_IDENTITY = 0, ORDER_AG_INTERLEAVE = 1, ORDER_ROTATE = 2 };
-enum RsMode : int { RS_NONE = 0, RS_ONESHOT = 1, RS_RING = 2 };
+// RS_DMA: the hybrid binding the paper benchmarks for GEMM+RS ("scatter is done using DMA, and
+// reduction is done on SMs"): remote partial tiles go to a local outbox, a per-(owner, 128-row block)
+// counter releases a flag, the copy engines move each finished block to the owner (host-enqueued
+// stream wait / memcpy / write-value), and the owner's epilogue reduces as in RS_ONESHOT.
+enum RsMode : int { RS_NONE = 0, RS_ONESHOT = 1, RS_RING = 2, RS_DMA = 3 };
 
 // Per rank driven by this launch (1 entry for a process-per-GPU comm, `world` for loopback).
 struct alignas(64) RankArgs {
@@ -64,6 +68,13 @@ struct alignas(64) Params {
   int debug_mode;
   uint32_t delay_ns, delay_seed;    // schedule perturbation (debug_delay, 0 = off)
   TraceBuf* trace;                  // device event trace (null = off)
+  // RS_DMA: local outbox [world * M_r, N] (tm_outbox), per (owner, 128-row block) counters and
+  // flags (local device memory; the host's copy streams wait on the flags)
+  CUtensorMap tm_outbox[kMaxWorld];
+  unsigned int* rs_cnt[kMaxWorld];
+  uint32_t* rs_ready[kMaxWorld];
+  unsigned int rs_cnt_target;       // increments per (owner, chunk) in one call
+  int rs_chunk_rows;                // RS_DMA granularity: rows per copy-engine chunk (multiple of 128)
   int topk;           // MoE: routed slots per token
   unsigned int moe_done_base;       // MoE scatter: counter value before this call
   uint32_t* moe_flags[kMaxWorld];   // MoE scatter: [W slots] completion flags of rank o

@@ -512,3 +512,51 @@ def test_binding_shape_and_dtype_checks(tl):
         c.gemm_rs(empty(256, 128).t(), empty(64, 256), empty(128, 64))
     with pytest.raises(ValueError, match="shape"):
         c.ag_gemm(X, empty(64, 128), empty(256, 32))                      # B rows != C cols
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_rs_dma_binding_matches_sm_binding(tl, W):
+    """GEMM-RS with the paper's hybrid binding (scatter on the copy engines, reduction on SMs,
+    rs_binding = 1): partial tiles go to a local outbox, the copy engines move each finished chunk to
+    its owner after a stream wait on the kernel's chunk flag, and the owner reduces exactly as in the
+    SM binding -> bitwise-identical results over epoch-cycling calls, for whole-block and 128-row
+    chunks, plus parity with the oracle."""
+    M, N, K = 256 * W, 384, 192
+    As, Bs = TI.gemm_rs_inputs(M, N, K, W, seed=W + 60)
+    a, b = [cuda(x) for x in As], [cuda(x) for x in Bs]
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=N)
+    ref = [empty(M // W, N) for _ in range(W)]
+    c.gemm_rs_lb(a, b, ref)
+    assert c.check()[0] == 0
+    c.set_option("rs_binding", 1)
+    for i, rows in enumerate([0, 128, 0, 256]):
+        c.set_option("rs_dma_rows", rows)
+        outs = [empty(M // W, N) for _ in range(W)]
+        c.gemm_rs_lb(a, b, outs)
+        st, diag = c.check()
+        assert st == 0, diag
+        for r in range(W):
+            assert torch.equal(outs[r], ref[r]), f"call {i} rank {r}"
+    oracle = O.gemm_rs([TI.to_f64(x) for x in As], [TI.to_f64(x) for x in Bs])
+    got = np.concatenate([f64(o) for o in ref], 0)
+    assert O.rel_frobenius(got, np.concatenate(oracle, 0)) < TOL
+
+
+def test_mlp_both_dma_bindings(tl):
+    """The whole layer with AllGather and scatter both on the copy engines (the paper's benchmarked
+    bindings) equals the all-SM layer bit for bit."""
+    W, M, H, I = 4, 1024, 256, 1024
+    X, G, U, W2 = TI.mlp_full(M, H, I, seed=9)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    args = ([cuda(x) for x in Xs], [cuda(w) for w in W1s], [cuda(w) for w in W2s])
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=H)
+    ref = [empty(M // W, H) for _ in range(W)]
+    c.mlp_forward_lb(*args, ref, act=TI.ACT_SILU_MUL)
+    c.set_option("ag_binding", 1)
+    c.set_option("rs_binding", 1)
+    for i in range(4):
+        outs = [empty(M // W, H) for _ in range(W)]
+        c.mlp_forward_lb(*args, outs, act=TI.ACT_SILU_MUL)
+        for r in range(W):
+            assert torch.equal(outs[r], ref[r]), f"call {i} rank {r}"
+    assert c.check()[0] == 0

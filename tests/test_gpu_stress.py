@@ -50,13 +50,18 @@ def test_perturbation_is_active(tl):
     assert slow > base + 0.05, (base, slow)
 
 
-@pytest.mark.parametrize("W,ring", [(2, 0), (4, 0), (8, 0), (4, 1), (8, 1)])
+@pytest.mark.parametrize("W,ring", [(2, 0), (4, 0), (8, 0), (4, 1), (8, 1), (4, "dma"), (8, "dma")])
 def test_mlp_bitwise_under_perturbed_schedules(tl, W, ring):
     M, H, I = 1024, 512, 2048
     X, G, U, W2 = TI.mlp_full(M, H, I, seed=11)
     Xs, W1s, W2s = (_cuda(L) for L in TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL))
     c = tl.Comm.loopback(W, 0, max_M=M, max_H=H)
-    c.set_option("rs_order", ring)
+    if ring == "dma":                               # both exchanges on the copy engines
+        c.set_option("ag_binding", 1)
+        c.set_option("rs_binding", 1)
+        c.set_option("rs_dma_rows", 128)
+    else:
+        c.set_option("rs_order", ring)
     c.set_option("comm_tile_rows", 32)            # many small producer tiles: many flags to race on
     outs = [torch.empty(M // W, H, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
     c.mlp_forward_lb(Xs, W1s, W2s, outs, act=TI.ACT_SILU_MUL)
