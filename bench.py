@@ -376,8 +376,9 @@ def main():
         o8 = [torch.empty(M_TOK // LW, HID, device="cuda", dtype=torch.bfloat16) for _ in range(LW)]
         z8 = [torch.empty(M_TOK, FFN // LW, device="cuda", dtype=torch.bfloat16) for _ in range(LW)]
 
-        def lb_time(binding):
+        def lb_time(binding, rs_binding=0):
             lc.set_option("ag_binding", binding)
+            lc.set_option("rs_binding", rs_binding)
             for _ in range(args.warmup):
                 lc.ag_gemm_lb(xs8, w18, z8, act=tl.ACT_SILU_MUL)
                 lc.gemm_rs_lb(z8, w28, o8)
@@ -422,8 +423,8 @@ def main():
                                                 "overlap_ms": round(ov, 4),
                                                 "ratio": round((cp + cm - ov) / cm, 4) if cm > 0 else None}
         lc.check()
-        for binding, name in ((0, "sm"), (1, "copy_engine")):
-            l1, l2, lst = lb_time(binding)
+        for binding, rsb, name in ((0, 0, "sm"), (1, 0, "copy_engine"), (1, 1, "copy_engine_ag_and_rs")):
+            l1, l2, lst = lb_time(binding, rsb)
             got = np.stack([o8[i // mr8][i % mr8].float().cpu().double().numpy() for i in rows])
             loop[f"ag_binding_{name}"] = {
                 "ag_gemm_ms": round(l1, 4), "gemm_rs_ms": round(l2, 4), "ms_per_step": round(l1 + l2, 4),

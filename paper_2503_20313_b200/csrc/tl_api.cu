@@ -751,6 +751,11 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
     if (st == TL_OK) st = get_write_value();
     p.rs_chunk_rows = (int)chunk;
     p.rs_cnt_target = (unsigned)((chunk / 128) * 4 * n_blocks * nsub);
+    // A chunk needs every remote tile of its rows, so every CTA must finish all its remote tiles
+    // before it can block on an own-block tile: one raster group per owner block (groups run in the
+    // rotated owner order r+1, ..., r), so all remote items precede all own items in item order.
+    // (The grouped raster interleaves owner blocks across n-blocks: measured deadlock at N >= 1536.)
+    p.raster_group = (M_r % (128 * pair) == 0) ? (int)(M_r / (128 * pair)) : 1;
   }
   if (comm) {
     for (int o = 0; o < W; ++o) {

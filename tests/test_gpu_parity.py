@@ -560,3 +560,26 @@ def test_mlp_both_dma_bindings(tl):
         for r in range(W):
             assert torch.equal(outs[r], ref[r]), f"call {i} rank {r}"
     assert c.check()[0] == 0
+
+
+@pytest.mark.parametrize("W,M,N", [(2, 2048, 2048), (4, 2048, 1536), (8, 4096, 4096)])
+def test_rs_dma_binding_many_items_per_cta(tl, W, M, N):
+    """Shapes where CTAs own several items: with the copy-engine scatter a chunk needs all of its
+    remote tiles, so the schedule must run every remote tile before any own-block tile (an
+    interleaved raster deadlocked here); bitwise equal to the SM binding."""
+    K = 192
+    As, Bs = TI.gemm_rs_inputs(M, N, K, W, seed=W + 70)
+    a, b = [cuda(x) for x in As], [cuda(x) for x in Bs]
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=N)
+    ref = [empty(M // W, N) for _ in range(W)]
+    c.gemm_rs_lb(a, b, ref)
+    c.set_option("rs_binding", 1)
+    c.set_option("timeout_ms", 5000)
+    for rows in (0, 128):
+        c.set_option("rs_dma_rows", rows)
+        outs = [empty(M // W, N) for _ in range(W)]
+        c.gemm_rs_lb(a, b, outs)
+        st, diag = c.check()
+        assert st == 0, diag
+        for r in range(W):
+            assert torch.equal(outs[r], ref[r])
