@@ -106,7 +106,8 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *   "copy_ctas"        CTAs per rank that run the AG copy role (default 0 = all)
  *   "rs_order"         0 = one-shot push to owner slots + fp32 owner reduce, 1 = ring (Fig. gemm_rs)
  *   "cta_pair"         2 = tcgen05 cta_group::2 (256-row tiles on an SM pair), 1 = single SM
- *   "raster_group"     m-blocks per rasterisation group (default 16)
+ *   "raster_group"     m-blocks per rasterisation group (default 0 = auto: 16, or one owner block
+ *                      for the ReduceScatter with world > 1)
  *   "num_ctas"         CTAs per rank (default: all SMs / local ranks, rounded to the pair size)
  *   "timeout_ms"       device-side flag-wait timeout (default 10000)
  *   "debug_drop_notify" (fault injection) index g >= 0 of one AG producer-tile notify to skip

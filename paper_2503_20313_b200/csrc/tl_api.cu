@@ -153,7 +153,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
-          raster_group = 16, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
+          raster_group = 0, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
           n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0;
 };
 
@@ -168,7 +168,7 @@ const OptDesc kOpts[] = {
     {"copy_ctas", &Options::copy_ctas, 0, 4096},
     {"rs_order", &Options::rs_order, 0, 1},
     {"cta_pair", &Options::cta_pair, 1, 2},
-    {"raster_group", &Options::raster_group, 1, 1 << 20},
+    {"raster_group", &Options::raster_group, 0, 1 << 20},
     {"num_ctas", &Options::num_ctas, 0, 4096},
     {"timeout_ms", &Options::timeout_ms, 1, 1ll << 40},
     {"debug_drop_notify", &Options::debug_drop_notify, -1, 1 << 30},
@@ -400,7 +400,7 @@ void fill_common(tl_comm* c, Params& p) {
   p.world = c->world;
   p.n_local = c->n_local;
   p.ctas_per_rank = ctas_per_rank(c);
-  p.raster_group = (int)c->opt.raster_group;
+  p.raster_group = c->opt.raster_group > 0 ? (int)c->opt.raster_group : 16;
   p.timeout_ns = (uint64_t)c->opt.timeout_ms * 1000000ull;
   p.diag = reinterpret_cast<Diag*>(c->ws[c->loopback ? 0 : c->rank] + c->lay.diag);
   p.drop_rank = (int)c->opt.debug_drop_rank;
@@ -737,6 +737,10 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
   set_items(p, nsub, p.ctas_per_rank / pair);
   const bool dma = comm && c->opt.rs_binding == 1;
   p.rs_mode = comm ? (dma ? RS_DMA : c->opt.rs_order == 1 ? RS_RING : RS_ONESHOT) : RS_NONE;
+  // default raster for the ReduceScatter: one group per owner block, so every remote partial leaves
+  // before any own-block tile waits for the peers' (the tile-order trade-off of P:313; 8 loopback
+  // ranks, 7B GEMM-RS: 0.84 ms vs 1.14 ms with 16-m-block groups, profiles/r01_rs_raster.log)
+  if (comm && c->opt.raster_group == 0 && M_r % (128 * pair) == 0) p.raster_group = (int)(M_r / (128 * pair));
   p.order = comm ? ORDER_ROTATE : ORDER_IDENTITY;
   p.tm_rows = 1;
   p.tiles_per_rank = 1;
