@@ -99,6 +99,20 @@ __device__ __forceinline__ void item_coords(const Params& p, int item, int& t, i
   }
 }
 
+// A whole 512-wide item whose second 256-column sub-tile lies entirely past N (the last n-block of a
+// ragged N) computes only its first sub-tile: every role (producer, MMA, epilogue) applies the same
+// clamp, so loads, MMAs, stores and RS flags stay consistent.  (The 7B TP-8 GEMM1, N_out = 1376,
+// wasted half of its last n-block: ~8 % of the MMAs.)
+template <int kNSub, int kEpi, int kMoE>
+__device__ __forceinline__ void clamp_subs(const Params& p, int nb, int sub_lo, int& sub_n) {
+  // (not for the ReduceScatter: its per-sub-tile flags must match across ranks whose schedules split
+  // different tiles)
+  if constexpr (kNSub == 2 && kMoE == MOE_NONE && kEpi != EPI_RS) {
+    constexpr int sub_w = (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) ? 128 : 256;   // output columns
+    if (sub_lo == 0 && sub_n == 2 && (nb * 2 + 1) * sub_w >= p.N_out) sub_n = 1;
+  }
+}
+
 // MoE work item -> (m-tile of the padded grouped rows, n-block, expert).  Tiles run in the order
 // of the device-built schedule (by the producer tile their last token needs, i.e. by expected
 // arrival), n-blocks innermost so a gathered A block is reused from L2.
@@ -342,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         item_coords<kNSub>(p, item, t, sub_lo, sub_n);
         if constexpr (kMoE == MOE_SCATTER) moe_coords(p, ra, item, mb, nb, expert);
         else tile_coords(p, rank, ra.m_rot, t, mb, nb);
+        clamp_subs<kNSub, kEpi, kMoE>(p, nb, sub_lo, sub_n);
         const int row0 = mb * BM + cta_in_pair * 128;
         if constexpr (kAG) {
           if (p.debug_mode != 1 && row0 < p.M) {
@@ -409,6 +424,11 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       for (int item = pair; item < total; item += n_pairs, ++it) {
         int t, sub_lo, sub_n;
         item_coords<kNSub>(p, item, t, sub_lo, sub_n);
+        if constexpr (kNSub == 2 && kMoE == MOE_NONE && kEpi != EPI_RS) {
+          int mb_, nb_;
+          tile_coords(p, rank, ra.m_rot, t, mb_, nb_);
+          clamp_subs<kNSub, kEpi, kMoE>(p, nb_, sub_lo, sub_n);
+        }
         const int as = it % kAccBufs;
         ptx::mbar_wait(&tempty[as], ((it / kAccBufs) & 1) ^ 1);
         ptx::tc_fence_after();
@@ -499,6 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       if constexpr (kMoE == MOE_SCATTER) mb = moe_scatter_tile(p, ra, item, nb);
       else if constexpr (kMoE) moe_coords(p, ra, item, mb, nb, expert);
       else tile_coords(p, rank, ra.m_rot, t, mb, nb);
+      clamp_subs<kNSub, kEpi, kMoE>(p, nb, sub_lo, sub_n);
       (void)expert;
       const int as = it % kAccBufs;
       ptx::mbar_wait(&tfull[as], (it / kAccBufs) & 1);
