@@ -370,7 +370,7 @@ void set_items(Params& p, int nsub, int n_pairs) {
 // 256-wide tiles (TMEM double-buffered, epilogue hidden) cost 1.12 per k-block (extra L2->SMEM
 // traffic); 512-wide tiles cost 2 per k-block plus ~9 for the un-overlapped epilogue; half items
 // (split tail) cost 1 per k-block plus ~4.5.
-int choose_nsub(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gated) {
+int choose_nsub(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gated, bool rs = false) {
   if (pair_of(c) != 2) return 1;
   if (c->opt.n_sub == 1 || c->opt.n_sub == 2) return (int)c->opt.n_sub;
   const int64_t P = ctas_per_rank(c) / 2;
@@ -381,8 +381,12 @@ int choose_nsub(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gate
   const int64_t T2 = m_blocks * ((N_out + 2 * bn1 - 1) / (2 * bn1));
   const double t1 = (double)((T1 + P - 1) / P) * 1.12 * kb;
   const int64_t rem = T2 % P;
-  const double full2 = 2.0 * kb + 9.0;
-  const double t2 = (double)(T2 / P) * full2 + (rem == 0 ? 0.0 : (2 * rem <= P ? kb + 4.5 : full2));
+  // un-overlapped epilogue of a 512-wide tile: ~9 k-blocks for the gated (activation) and the
+  // reduce-scatter epilogues, ~3.5 for a plain store (refit on the TP-2..8 rank shapes:
+  // profiles/r01_nsub_ab.log, 512-wide 3-8 % faster where the old constant chose 256-wide)
+  const double epi = (gated || rs) ? 9.0 : 3.5;
+  const double full2 = 2.0 * kb + epi;
+  const double t2 = (double)(T2 / P) * full2 + (rem == 0 ? 0.0 : (2 * rem <= P ? kb + epi / 2 : full2));
   return t2 < t1 ? 2 : 1;
 }
 
@@ -700,7 +704,7 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
   if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31)) return fail(TL_ERR_UNSUPPORTED, "dimension >= 2^31");
   const int64_t M_r = M / W;
   const int pair = pair_of(c);
-  const int nsub = choose_nsub(c, M, N, K, false);
+  const int nsub = choose_nsub(c, M, N, K, false, W > 1);
   const int64_t n_blocks = (N + 256 * nsub - 1) / (256 * nsub);
   if (W > 1) {
     if (M_r % 128) return fail(TL_ERR_UNSUPPORTED, "GEMM-RS with world > 1 needs (M/world) %% 128 == 0 (M/world=%lld)",
