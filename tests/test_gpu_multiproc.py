@@ -85,7 +85,7 @@ def test_two_processes_ipc_mlp():
         assert all(np.array_equal(outs[0], o) for o in outs[1:])
 
 
-def _worker_all(rank, world, port, q):
+def _worker_all(rank, world, port, q, dma=False):
     """One rank per process: the MLP layer, the MoE layer and SP attention through the
     process-group comm (IPC-mapped peers), results sent back for the oracle check."""
     import torch.distributed as dist
@@ -103,6 +103,9 @@ def _worker_all(rank, world, port, q):
         comm = tl.Comm.from_process_group(None, 0, max_M=max(M, 512 * world), max_H=512, max_topk=2)
         comm.set_option("num_ctas", max(2, 148 // world // 2 * 2))
         comm.set_option("timeout_ms", 120000)
+        if dma:   # both exchanges on the copy engines (cross-process IPC copies + stream flags)
+            comm.set_option("ag_binding", 1)
+            comm.set_option("rs_binding", 1)
         out = torch.empty(M // world, H, device="cuda", dtype=torch.bfloat16)
         comm.mlp_forward(Xs[rank].cuda(), W1s[rank].cuda(), W2s[rank].cuda(), out, act=tl.ACT_SILU_MUL)
         res["mlp"] = out.float().cpu().numpy()
@@ -138,8 +141,8 @@ def _worker_all(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_processes_ipc_all_ops(world):
+@pytest.mark.parametrize("world,dma", [(2, False), (4, False), (2, True)])
+def test_processes_ipc_all_ops(world, dma):
     """Every fused op over real processes (one rank each, CUDA IPC peers; the GPU is time-shared)."""
     import torch.multiprocessing as mp
     import tl_inputs as TI
@@ -147,7 +150,7 @@ def test_processes_ipc_all_ops(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_all, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker_all, args=(r, world, port, q, dma)) for r in range(world)]
     for p in procs:
         p.start()
     got = {}
