@@ -501,7 +501,7 @@ def run_attention(args, helpers):
                      "frac_sustained": round(ach / P_sust, 4), "peak_source": peak_src,
                      "traffic": _traffic("attention_bytes") if W == 1 else None,
                      "per_launch_flop": fl,
-                     "note": "MUFU exp2 (16/clk/SM) co-limits: 128x128 scores per 2 x 128^3 MMA FLOPs"},
+                     "note": "bound by the per-tile chain softmax -> P.V -> Q.K^T (~2900 vs 2048 MMA cycles per KV block; DESIGN.md 7), MUFU ~50 % busy"},
         "cpu_baseline": cpu,
         "e2e": {"value": round(fl * W / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
                 "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": pipe.bytes_in,
