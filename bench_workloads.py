@@ -275,12 +275,14 @@ def run_moe(args, helpers):
             ob.copy_(part)
         if ev:
             ev[1].record(stream)
-    b_total, _ = _timed(base_step, args.steps, args.warmup, barrier, stream, 2)
-    bms = max_over_ranks(b_total) / args.steps
+    bms = None
+    if not args.no_baseline:
+        b_total, _ = _timed(base_step, args.steps, args.warmup, barrier, stream, 2)
+        bms = max_over_ranks(b_total) / args.steps
 
     # vLLM's fused MoE kernel (the paper's MoE baseline) on this rank's local problem
     vllm = None
-    if not distributed:
+    if not distributed and not args.no_baseline:
         try:
             from vllm.model_executor.layers.fused_moe import fused_experts
             xv = X.cuda()
@@ -325,10 +327,11 @@ def run_moe(args, helpers):
         "clocks": clk,
         "parity": parity,
         "baseline_vllm": vllm,
-        "baseline_torch": {"impl": "torch index_select + per-expert cuBLAS + silu*mul + per-expert cuBLAS + "
-                                   "weighted index_add (+ NCCL all_gather / reduce_scatter for W > 1)",
-                           "ms_per_step": round(bms, 4), "value": round((f1 + f2) * W / (bms * 1e-3) / 1e12, 2),
-                           "unit": "TFLOPS", "speedup_ours": round(bms / ms, 4)},
+        "baseline_torch": None if bms is None else {
+            "impl": "torch index_select + per-expert cuBLAS + silu*mul + per-expert cuBLAS + weighted index_add "
+                    "(+ NCCL all_gather / reduce_scatter for W > 1)",
+            "ms_per_step": round(bms, 4), "value": round((f1 + f2) * W / (bms * 1e-3) / 1e12, 2),
+            "unit": "TFLOPS", "speedup_ours": round(bms / ms, 4)},
     })
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -441,14 +444,16 @@ def run_attention(args, helpers):
                                                          vt.transpose(0, 1).unsqueeze(0))
         if ev:
             ev[1].record(stream)
-    b_total, _ = _timed(base_step, args.steps, args.warmup, barrier, stream, 2)
-    bms = max_over_ranks(b_total) / args.steps
+    bms = None
+    if not args.no_baseline:
+        b_total, _ = _timed(base_step, args.steps, args.warmup, barrier, stream, 2)
+        bms = max_over_ranks(b_total) / args.steps
 
     # overlap ratio of the fused AllGather-KV + attention (the paper's attention metric):
     # W = 8 ranks emulated on this GPU; comp_only = the same launch without K/V traffic or waits,
     # comm_only = only the copy role, overlap = the normal launch
     loop = None
-    if not distributed:
+    if not distributed and not args.no_loopback:
         LW = 8
         lc = tl.Comm.loopback(LW, dev, S, 2 * h * D)
         lQs, lKs, lVs = ([t.cuda() for t in L] for L in TI.attention_inputs(S, h, D, LW, seed=0))
@@ -512,10 +517,10 @@ def run_attention(args, helpers):
         "clocks": clk,
         "parity": parity,
         "loopback_w8": loop,
-        "baseline_torch": {"impl": "torch SDPA (cuDNN/flash backend as torch selects) (+ NCCL all_gather "
-                                   "of K and V for W > 1)", "ms_per_step": round(bms, 4),
-                           "value": round(fl * W / (bms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
-                           "speedup_ours": round(bms / ms, 4)},
+        "baseline_torch": None if bms is None else {
+            "impl": "torch SDPA (cuDNN/flash backend as torch selects) (+ NCCL all_gather of K and V for W > 1)",
+            "ms_per_step": round(bms, 4), "value": round(fl * W / (bms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
+            "speedup_ours": round(bms / ms, 4)},
     })
     if rank == 0:
         print(json.dumps(line), flush=True)
