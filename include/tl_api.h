@@ -245,13 +245,14 @@ tl_status tl_moe_gemm_rs_loopback(tl_comm_t comm, const void* const* Zg, const i
  * V = AllGather_rows(V_shard), per head, non-causal.
  *   Q_shard, K_shard, V_shard, O_shard: device bf16, row-major [S/world, heads, head_dim]
  *     (token-major, heads interleaved; the usual [tokens, heads*d] projection output), caller-owned.
- *   S: total sequence length; head_dim must be 128; S/world must be a multiple of 128; scale > 0.
+ *   S: total sequence length, a multiple of world (ragged S/world and S % 128 != 0 are handled by a
+ *   masking kernel variant); head_dim must be 128; scale > 0.
  * The gathered K and V live in the comm workspace (bank of the AG epoch): 2*S*heads*head_dim must
  * not exceed max_M*max_H of the comm.  Each rank's kernel pushes its K/V producer tiles to every
  * rank (bulk copies over NVLink) and releases a per-tile flag; the attention CTAs wait the flags
  * of the KV blocks they reach, own shard first.  fp32 softmax statistics and accumulation; one
  * bf16 rounding of O.  Errors: TL_ERR_INVALID (shape/alignment/capacity), TL_ERR_UNSUPPORTED
- * (head_dim != 128, S/world % 128 != 0), TL_ERR_CUDA; a lost peer shows up in tl_comm_check. */
+ * (head_dim != 128), TL_ERR_CUDA; a lost peer shows up in tl_comm_check. */
 tl_status tl_sp_attention(tl_comm_t comm, const void* Q_shard, const void* K_shard, const void* V_shard,
                           void* O_shard, int64_t S, int heads, int head_dim, float scale, void* stream);
 tl_status tl_sp_attention_loopback(tl_comm_t comm, const void* const* Q_shard, const void* const* K_shard,

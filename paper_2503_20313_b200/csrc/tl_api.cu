@@ -1382,7 +1382,6 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
   if (S % W) return fail(TL_ERR_INVALID, "S=%lld not divisible by world=%d", (long long)S, W);
   if (D != 128) return fail(TL_ERR_UNSUPPORTED, "head_dim must be 128 (got %d)", D);
   const int64_t S_r = S / W;
-  if (S_r % 128) return fail(TL_ERR_UNSUPPORTED, "S/world must be a multiple of 128 (S/world=%lld)", (long long)S_r);
   if (heads > 65535 || S >= (1ll << 31)) return fail(TL_ERR_UNSUPPORTED, "shape too large");
   const int64_t row_elems = (int64_t)heads * D;
   if (W > 1 && 2 * S * row_elems > c->max_M * c->max_H)
@@ -1483,6 +1482,8 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
                             tl_attn_kernel<true, 4>, tl_attn_kernel<true, 6>, tl_attn_kernel<true, 8>)
                      : pick(tl_attn_kernel<false, 0>, tl_attn_kernel<false, 2>, tl_attn_kernel<false, 3>,
                             tl_attn_kernel<false, 4>, tl_attn_kernel<false, 6>, tl_attn_kernel<false, 8>);
+    // ragged sequence shards (S/world % 128 != 0): the masking instantiation (default exp2 split only)
+    if (S_r % 128) kern = comm ? tl_attn_kernel<true, 3, true> : tl_attn_kernel<false, 3, true>;
     const int smem = comm ? AttnLayout<true>::smem_request : AttnLayout<false>::smem_request;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) {

@@ -275,7 +275,8 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar) {
       : "memory");
 }
 
-template <bool kAG, int kPolyMod>
+// kRagged: S/world % 128 != 0 (a separate instantiation, so the aligned kernel's code is unchanged).
+template <bool kAG, int kPolyMod, bool kRagged = false>
 __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_constant__ AttnParams p) {
   using L = AttnLayout<kAG>;
   extern __shared__ uint8_t smem_raw[];
@@ -285,11 +286,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
   const int cta = blockIdx.x % p.ctas_per_rank;
   const AttnRank& ra = p.rk[lr];
   const int rank = ra.rank;
-  const int nqb = p.S_r / 128, npairs = (nqb + 1) / 2, n_units = p.debug_mode == 2 ? 0 : p.heads * npairs;
-  const int n_kv = p.S / 128, bpr = p.S_r / 128;
+  const int nqb = (p.S_r + 127) / 128, npairs = (nqb + 1) / 2, n_units = p.debug_mode == 2 ? 0 : p.heads * npairs;
+  const int n_kv = (p.S + 127) / 128, bpr = p.S_r / 128;
   // consumption order interleaves the shards block by block (see attn_kv_block); independent of the
-  // producer tile height, so the decoupled comm tile size never changes the result
+  // producer tile height, so the decoupled comm tile size never changes the result.
+  // kRagged: KV blocks straddle shards, so they are visited in sequence order from the block holding
+  // this rank's first row; the last block (S % 128 valid keys when S % 128 != 0) is loaded with TMA
+  // zero fill and its missing keys are masked to -inf; a partial last query tile stores its valid rows.
   const int bpc = 1;
+  const int kv_first = kRagged ? (int)(((long long)rank * p.S_r) / 128) : 0;
+  const int kv_tail = p.S - (n_kv - 1) * 128;                       // valid keys in block n_kv - 1
+  const int j_mask = kv_tail < 128 ? (n_kv - 1 - kv_first + n_kv) % n_kv : -1;   // visit index of that block
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::off_bar);
   uint64_t* q_full = bars + 0;    // [2] per tile
@@ -350,10 +357,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
           ptx::tma_load_3d<1>(&ra.tm_q, &q_full[x], q + 16384, 64, h, qb * 128);
         }
         for (int j = 0; j < n_kv; ++j, ++g) {
-          const int kvb = attn_kv_block(j, rank, p.world, bpr, bpc);
+          const int kvb = kRagged ? (j + kv_first) % n_kv : attn_kv_block(j, rank, p.world, bpr, bpc);
           if constexpr (kAG) {
             debug_delay(p.delay_ns, p.delay_seed, rank, 2 * j + 1);
-            if (p.debug_mode != 1) attn_wait_rows(p, rank, kvb * 128, kvb * 128 + 128);
+            if (p.debug_mode != 1) attn_wait_rows(p, rank, kvb * 128, min(kvb * 128 + 128, p.S));
           }
           const int st = g & 1;
           const uint32_t ph = (g >> 1) & 1;
@@ -519,6 +526,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
 #pragma unroll
         for (int k = 0; k < 4; ++k) ptx::tmem_ld32(t_s + k * 32, s + 32 * k);
         ptx::tmem_ld_wait_fence<128>(s);
+        if constexpr (kRagged) {
+          if (j == j_mask) {   // keys beyond S (zero-filled rows) get weight 0
+#pragma unroll
+            for (int i = 0; i < 128; ++i)
+              if (i >= kv_tail) s[i] = -INFINITY;
+          }
+        }
         // row max: 8 independent FMNMX3 chains
         float mc[8];
 #pragma unroll
@@ -593,7 +607,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
       ++o_cnt;
       ptx::tc_fence_after();
       const float inv = 1.f / l;
-      if (store) {
+      if (store) {   // warp-uniform: tcgen05.ld below is a warp-collective (.sync.aligned) instruction
+        const bool row_ok = !kRagged || qb * 128 + ew * 32 + (int)lane < p.S_r;   // rows of a partial last tile
         uint8_t* orow = ra.o + ((size_t)(qb * 128 + ew * 32 + lane) * p.heads + h) * 256;
 #pragma unroll 1
         for (int k = 0; k < 4; ++k) {
@@ -605,7 +620,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
             const float* w = o + 8 * v;
             uint4 val = make_uint4(cvt_bf16x2(w[0] * inv, w[1] * inv), cvt_bf16x2(w[2] * inv, w[3] * inv),
                                    cvt_bf16x2(w[4] * inv, w[5] * inv), cvt_bf16x2(w[6] * inv, w[7] * inv));
-            *reinterpret_cast<uint4*>(orow + k * 64 + v * 16) = val;
+            if (row_ok) *reinterpret_cast<uint4*>(orow + k * 64 + v * 16) = val;
           }
         }
       }

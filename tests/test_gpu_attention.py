@@ -62,6 +62,49 @@ def test_attention_w1(tl, S, heads):
     assert _err(results[0], ref) < TOL
 
 
+@pytest.mark.parametrize("W,S", [(1, 1), (1, 100), (1, 200), (1, 333), (1, 1000), (2, 200), (2, 384), (3, 450),
+                                 (4, 400), (8, 576), (8, 8 * 200)])
+def test_attention_ragged(tl, W, S):
+    """Ragged shapes (the masking kernel variant): S % 128 != 0 (the last KV block is loaded with TMA
+    zero fill and its missing keys are masked to -inf), S/world % 128 != 0 (KV blocks straddle shards;
+    the last query tile is partial, with rows split inside a warp, and only valid rows are stored),
+    S/world < 128, and a single token."""
+    results, ref = _run(tl, W, S, 3)
+    assert _err(results[0], ref) < TOL
+
+
+def test_attention_ragged_no_store_beyond_rows(tl):
+    """A partial last query tile writes only its S_r rows: the bytes after O are left untouched."""
+    S, heads = 200, 2
+    Qs, Ks, Vs = TI.attention_inputs(S, heads, 128, 1, seed=3)
+    comm = _comm(tl, 1, S, heads)
+    big = torch.full((S + 128, heads, 128), 7.0, device="cuda", dtype=torch.bfloat16)
+    tl.sp_attention(comm, Qs[0].cuda(), Ks[0].cuda(), Vs[0].cuda(), big[:S])
+    assert comm.check()[0] == 0
+    assert torch.all(big[S:] == 7.0)
+    f = lambda L: [TI.to_f64(t) for t in L]
+    ref = O.sp_attention(f(Qs), f(Ks), f(Vs), 128 ** -0.5)
+    assert _err([big[:S]], ref) < TOL
+
+
+@pytest.mark.parametrize("binding", [0, 1])
+def test_attention_ragged_tile_height_invariance(tl, binding):
+    """Ragged shards (S/world = 200): the result does not depend on the producer tile height or on the
+    resource binding of the K/V AllGather."""
+    W, S, heads = 2, 400, 2
+    inputs = TI.attention_inputs(S, heads, 128, W, seed=9)
+    outs = []
+    for rows in (16, 64, 200):
+        comm = _comm(tl, W, S, heads)
+        comm.set_option("comm_tile_rows", rows)
+        comm.set_option("dma_tile_rows", rows)
+        comm.set_option("ag_binding", binding)
+        results, ref = _run(tl, W, S, heads, comm=comm, inputs=inputs)
+        outs.append(torch.cat(results[0], 0))
+    assert _err(results[0], ref) < TOL
+    assert all(torch.equal(o, outs[0]) for o in outs)
+
+
 @pytest.mark.parametrize("W", [2, 4, 8])
 def test_attention_loopback(tl, W):
     results, ref = _run(tl, W, 256 * W, 2)
@@ -151,9 +194,6 @@ def test_attention_validation(tl):
     q = torch.zeros(128, 2, 64, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(tl.TLError):
         tl.sp_attention(comm, q, q, q, torch.empty_like(q))           # head_dim 64
-    q = torch.zeros(100, 2, 128, device="cuda", dtype=torch.bfloat16)
-    with pytest.raises(tl.TLError):
-        tl.sp_attention(comm, q, q, q, torch.empty_like(q))           # S not a multiple of 128
     q = torch.zeros(128, 2, 128, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(tl.TLError):
         tl.sp_attention(comm, q, q, q, torch.empty_like(q), scale=-1.0)
