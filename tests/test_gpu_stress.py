@@ -158,9 +158,9 @@ def test_moe_layer_bitwise_under_perturbed_schedules(tl, W):
                 assert torch.equal(got[r], ref[r]), f"delay {d} call {call} rank {r}"
 
 
-@pytest.mark.parametrize("W", [2, 4])
-def test_attention_bitwise_under_perturbed_schedules(tl, W):
-    S, heads = 512 * W, 2
+@pytest.mark.parametrize("W,s_r", [(2, 512), (4, 512), (4, 200)])
+def test_attention_bitwise_under_perturbed_schedules(tl, W, s_r):
+    S, heads = s_r * W, 2          # s_r = 200: the ragged (masking) kernel, KV blocks straddling shards
     Qs, Ks, Vs = (_cuda(L) for L in TI.attention_inputs(S, heads, 128, W, seed=8))
     c = tl.Comm.loopback(W, 0, max_M=S, max_H=2 * heads * 128)
     c.set_option("comm_tile_rows", 32)
