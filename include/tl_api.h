@@ -98,7 +98,9 @@ tl_status tl_comm_destroy(tl_comm_t comm);
 /* rank (-1 for loopback), world, number of ranks driven by this process (1 or world). */
 tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
 
-/* Options (the decoupled design space), each also settable by env TL_<KEY upper>:
+/* Options (the decoupled design space).  The tunables are also read from the environment
+ * (TL_<KEY upper>) when the comm is created; the debug / fault-injection options (debug_mode,
+ * debug_drop_notify, debug_drop_rank, debug_delay_ns) are NOT: only tl_set_option sets them.
  *   "comm_tile_rows"   Tm_p, rows per AG producer tile (default 64; 16..M/world)
  *   "channels_per_rank" C, barrier channels per rank (default 0 = one per producer tile);
  *                      a consumer tile waits on every producer tile of every channel its rows
@@ -138,7 +140,9 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *   "pdl"              programmatic dependent launch of the GEMM kernels (default 1): their prologue
  *                      may overlap the previous kernel in the stream (they wait before any data access)
  *   "attn_poly"        tl_sp_attention: every n-th pair of exponentials is evaluated on the FMA pipe
- *                      (Cody-Waite + cubic) instead of MUFU (default 3; 0 = all on MUFU; 2,3,4,6,8) */
+ *                      (Cody-Waite + cubic) instead of MUFU (default 3; 0 = all on MUFU; 2,3,4,6,8).
+ *                      Ragged shapes (S/world % 128 != 0) always use the default split (3); the
+ *                      option affects speed only, never results beyond rounding. */
 tl_status tl_set_option(tl_comm_t comm, const char* key, int64_t value);
 tl_status tl_get_option(tl_comm_t comm, const char* key, int64_t* value);
 

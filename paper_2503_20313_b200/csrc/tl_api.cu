@@ -218,8 +218,12 @@ struct tl_comm {
 
 namespace {
 
+// Tunables may come from the environment (TL_<KEY upper>); the debug / fault-injection switches
+// (debug_mode, debug_drop_*, debug_delay_ns) never do: they change results or timing on purpose, so only an
+// explicit tl_set_option call can turn them on.
 void apply_env(Options& o) {
   for (const auto& d : kOpts) {
+    if (!strncmp(d.key, "debug_", 6)) continue;
     std::string env = "TL_";
     for (const char* c = d.key; *c; ++c) env += (char)toupper(*c);
     const char* v = getenv(env.c_str());
@@ -268,11 +272,9 @@ tl_status launch_t(tl_comm* c, const Params& p, cudaStream_t stream) {
   constexpr int kStages = stages_for(kPair, kAG, kNSub);
   using L = Layout<kPair, kStages, kAG, kNSub>;
   auto kern = tl_gemm_kernel<kPair, kStages, kEpi, kAG, kNSub, kMoE>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::smem_request));
-    attr_set = true;
-  }
+  // set on every launch: the attribute lives in the current device's context (a comm on a second device
+  // needs it too), and the call is cheap next to the launch
+  TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::smem_request));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_local * p.ctas_per_rank);
   cfg.blockDim = dim3(kThreads);
@@ -526,6 +528,9 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   if (W > 1 && sm.tiles_per_rank > kAgFlagStride)
     return fail(TL_ERR_UNSUPPORTED, "too many producer tiles per rank (%d > %d): raise comm_tile_rows",
                 sm.tiles_per_rank, kAgFlagStride);
+  if ((int64_t)sm.Tm * K * 2 >= (1ll << 31))   // the copy role counts a producer tile's bytes in 32 bits
+    return fail(TL_ERR_UNSUPPORTED, "producer tile of %d rows x %lld bytes >= 2 GiB: lower comm_tile_rows", sm.Tm,
+                (long long)(K * 2));
   if (moe && K == 0) return fail(TL_ERR_UNSUPPORTED, "MoE with K == 0");
   if (M == 0 || N_out == 0) return TL_OK;
   if (K == 0) {
@@ -1403,6 +1408,9 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
                                  (int)c->opt.channels_per_rank);
   if (W > 1 && sm.tiles_per_rank > kAgFlagStride)
     return fail(TL_ERR_UNSUPPORTED, "too many producer tiles per rank (%d): raise comm_tile_rows", sm.tiles_per_rank);
+  if ((int64_t)sm.Tm * row_bytes >= (1ll << 31))   // the copy role counts a producer tile's bytes in 32 bits
+    return fail(TL_ERR_UNSUPPORTED, "producer tile of %d rows x %lld bytes >= 2 GiB: lower comm_tile_rows", sm.Tm,
+                (long long)row_bytes);
   TL_CUDA(cudaSetDevice(c->device));
   const bool comm = W > 1;
   const uint32_t epoch = comm ? ++c->ag_epoch : 0;

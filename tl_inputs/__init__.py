@@ -30,20 +30,25 @@ ACT_GELU_TANH_MUL = 2
 _TID_X, _TID_G, _TID_U, _TID_W2, _TID_A, _TID_B = 0, 1, 2, 3, 4, 5
 
 
-def _randn(shape, seed: int, tid: int, std: float = 1.0) -> torch.Tensor:
-    g = torch.Generator().manual_seed(int(seed) * 1000 + tid)
-    t = torch.randn(*shape, generator=g, dtype=torch.float32)
+def _randn(shape, seed: int, tid: int, std: float = 1.0, device=None) -> torch.Tensor:
+    """Seeded N(0, std^2) draw rounded to bf16.  `device=None`: CPU generator (the tests' recipe);
+    a CUDA device: the same recipe with that device's (Philox) generator -- a different but equally
+    seeded stream, identical on every rank that draws it (bench.py's large shapes)."""
+    dev = torch.device("cpu") if device is None else torch.device(device)
+    g = torch.Generator(device=dev).manual_seed(int(seed) * 1000 + tid)
+    t = torch.randn(*shape, generator=g, dtype=torch.float32, device=dev)
     if std != 1.0:
         t.mul_(std)
     return t.to(torch.bfloat16)
 
 
-def mlp_full(M: int, H: int, I: int, seed: int = 0):
-    """Full (unsharded) LLaMA-style MLP problem: X [M,H], G [I,H], U [I,H], W2 [H,I], bf16 CPU."""
-    X = _randn((M, H), seed, _TID_X)
-    G = _randn((I, H), seed, _TID_G, H ** -0.5)
-    U = _randn((I, H), seed, _TID_U, H ** -0.5)
-    W2 = _randn((H, I), seed, _TID_W2, I ** -0.5)
+def mlp_full(M: int, H: int, I: int, seed: int = 0, device=None):
+    """Full (unsharded) LLaMA-style MLP problem: X [M,H], G [I,H], U [I,H], W2 [H,I], bf16 (CPU, or drawn
+    on `device`)."""
+    X = _randn((M, H), seed, _TID_X, device=device)
+    G = _randn((I, H), seed, _TID_G, H ** -0.5, device=device)
+    U = _randn((I, H), seed, _TID_U, H ** -0.5, device=device)
+    W2 = _randn((H, I), seed, _TID_W2, I ** -0.5, device=device)
     return X, G, U, W2
 
 
