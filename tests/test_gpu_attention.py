@@ -11,6 +11,7 @@ import torch
 
 import tl_inputs as TI
 from oracle import tl_oracle as O
+from parity import assert_parity
 
 pytestmark = pytest.mark.gpu
 TOL = 5e-3
@@ -52,8 +53,10 @@ def _run(tl, W, S, heads, scale=None, seed=0, comm=None, calls=1, inputs=None):
 
 
 def _err(outs, ref):
+    """Element-wise parity (tests/parity.py: global, per 128-row tile, per (token, head) row, per element);
+    returns the global relative Frobenius error."""
     got = np.concatenate([o.float().cpu().double().numpy() for o in outs], 0)
-    return O.rel_frobenius(got, np.concatenate(ref, 0))
+    return assert_parity(got, np.concatenate(ref, 0))["global"]
 
 
 @pytest.mark.parametrize("S,heads", [(128, 1), (256, 3), (1024, 4)])
@@ -224,7 +227,7 @@ def test_attention_paper_shape_attn1_16k_sampled(tl):
         q = TI.to_f64(Qs[r])[rows]
         ref = O.sp_attention([q], [K64], [V64], D ** -0.5)[0]
         got = outs[r][torch.as_tensor(rows, device="cuda")].float().cpu().double().numpy()
-        assert O.rel_frobenius(got, ref) < TOL
+        assert_parity(got, ref)
 
 
 def test_attention_bench_config_w1_sampled(tl):
@@ -244,7 +247,7 @@ def test_attention_bench_config_w1_sampled(tl):
     K64, V64 = TI.to_f64(Ks[0]), TI.to_f64(Vs[0])
     ref = O.sp_attention([TI.to_f64(Qs[0])[rows]], [K64], [V64], D ** -0.5)[0]
     got = o[torch.as_tensor(rows, device="cuda")].float().cpu().double().numpy()
-    assert O.rel_frobenius(got, ref) < TOL
+    assert_parity(got, ref)
 
 
 @pytest.mark.parametrize("W", [2, 4, 8])

@@ -8,6 +8,7 @@ import torch
 
 import tl_inputs as TI
 from oracle import tl_oracle as O
+from parity import assert_parity
 
 pytestmark = pytest.mark.gpu
 TOL = 5e-3
@@ -64,7 +65,7 @@ def _check(ref_rows, ref_Y, Ys, rows, offs, topk, exact=False):
         if exact:
             assert np.array_equal(got, ref_Y[r])
         else:
-            assert O.rel_frobenius(got, ref_Y[r]) < TOL
+            assert_parity(got, ref_Y[r])
 
 
 @pytest.mark.parametrize("W", [1, 2, 4, 8])
@@ -146,7 +147,7 @@ def test_moe_layer_parity(tl, W, topk):
     """Full TP MoE FFN: AG + Gather + GroupGEMM + SiLU*up, then GroupGEMM + Scatter + TopK + RS."""
     results, ref = _moe_layer(tl, W, M=256 * W if W > 1 else 512, H=256, I=256 * W, E=8, topk=topk)
     got = np.concatenate([o.float().cpu().double().numpy() for o in results[0]], 0)
-    assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
+    assert_parity(got, np.concatenate(ref, 0))
 
 
 @pytest.mark.parametrize("pair,nsub", [(1, 1), (2, 1), (2, 2)])
@@ -155,7 +156,7 @@ def test_moe_layer_options_and_epochs(tl, pair, nsub):
     epochs cycling, completion counters accumulating) are bitwise identical."""
     results, ref = _moe_layer(tl, 4, M=1024, H=512, I=1024, E=16, topk=3, skew=1.0, calls=4, pair=pair, nsub=nsub)
     got = np.concatenate([o.float().cpu().double().numpy() for o in results[0]], 0)
-    assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
+    assert_parity(got, np.concatenate(ref, 0))
     for later in results[1:]:
         for a, b in zip(later, results[0]):
             assert torch.equal(a, b)
@@ -172,7 +173,7 @@ def test_moe_layer_copy_engine_binding(tl, W):
         for a, b in zip(call, sm_res[0]):
             assert torch.equal(a, b)
     got = np.concatenate([o.float().cpu().double().numpy() for o in dma_res[-1]], 0)
-    assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
+    assert_parity(got, np.concatenate(ref, 0))
 
 
 def test_moe_layer_single_expert_matches_dense_mlp_kernels(tl):
@@ -180,7 +181,7 @@ def test_moe_layer_single_expert_matches_dense_mlp_kernels(tl):
     W, M, H, I = 2, 512, 256, 512
     results, ref = _moe_layer(tl, W, M, H, I, E=1, topk=1)
     got = np.concatenate([o.float().cpu().double().numpy() for o in results[0]], 0)
-    assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
+    assert_parity(got, np.concatenate(ref, 0))
 
 
 def test_moe_layer_bench_config_w1_sampled(tl):
@@ -204,4 +205,4 @@ def test_moe_layer_bench_config_w1_sampled(tl):
     f = lambda L: [TI.to_f64(t) for t in L]
     ref = BW._moe_oracle_tokens(X, ids, wts, f(W1s), f(W2s), toks)
     got = out[torch.as_tensor(toks, device="cuda")].float().cpu().double().numpy()
-    assert O.rel_frobenius(got, ref) < 5e-3
+    assert_parity(got, ref)

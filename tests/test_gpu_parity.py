@@ -11,6 +11,7 @@ import torch
 
 import tl_inputs as TI
 from oracle import tl_oracle as O
+from parity import assert_parity
 
 pytestmark = pytest.mark.gpu
 TOL = 5e-3
@@ -47,7 +48,7 @@ def test_gemm_w1_plain(tl, pair, nsub, M, N, K):
     c.ag_gemm(cuda(A[0]), cuda(Bs[0]), C)
     torch.cuda.synchronize()
     _, ref = O.ag_gemm([TI.to_f64(A[0])], [TI.to_f64(Bs[0])])
-    assert O.rel_frobenius(f64(C), ref[0]) < TOL
+    assert_parity(f64(C), ref[0])
 
 
 @pytest.mark.parametrize("pair,nsub", [(1, 1), (2, 1), (2, 2)])
@@ -63,7 +64,7 @@ def test_gemm_w1_gated(tl, pair, nsub, act, M, N, K):
     torch.cuda.synchronize()
     _, Y = O.ag_gemm([TI.to_f64(A[0])], [TI.to_f64(Bs[0])])
     ref = O.activation(Y[0], act)
-    assert O.rel_frobenius(f64(C), ref) < TOL
+    assert_parity(f64(C), ref)
 
 
 def test_gemm_k0_and_empty(tl):
@@ -129,7 +130,7 @@ def test_ag_gemm_random(tl, W, act, nsub):
     assert st == 0, diag
     _, Y = O.ag_gemm([TI.to_f64(a) for a in As], [TI.to_f64(b) for b in Bs])
     for r in range(W):
-        assert O.rel_frobenius(f64(Cs[r]), O.activation(Y[r], act)) < TOL
+        assert_parity(f64(Cs[r]), O.activation(Y[r], act))
 
 
 @pytest.mark.parametrize("W", [2, 3])
@@ -145,7 +146,7 @@ def test_ag_gemm_ragged_rank_rows(tl, W):
     assert st == 0, diag
     _, Y = O.ag_gemm([TI.to_f64(a) for a in As], [TI.to_f64(b) for b in Bs])
     for r in range(W):
-        assert O.rel_frobenius(f64(Cs[r]), Y[r]) < TOL
+        assert_parity(f64(Cs[r]), Y[r])
 
 
 def test_ag_decoupling_soundness(tl):
@@ -203,7 +204,7 @@ def test_gemm_rs_random(tl, W, ring, nsub):
     assert st == 0, diag
     ref = O.gemm_rs([TI.to_f64(a) for a in As], [TI.to_f64(b) for b in Bs])
     got = np.concatenate([f64(x) for x in Cs], 0)
-    assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
+    assert_parity(got, np.concatenate(ref, 0))
 
 
 def test_gemm_rs_deterministic(tl):
@@ -249,7 +250,7 @@ def test_mlp_tiny_config(tl, W, act, nsub):
     Xs, W1s, W2s, outs = _mlp_case(tl, W, M, H, I, act, nsub=nsub)
     ref = O.mlp_forward([TI.to_f64(x) for x in Xs], [TI.to_f64(w) for w in W1s], [TI.to_f64(w) for w in W2s], act)
     got = np.concatenate([f64(o) for o in outs], 0)
-    assert O.rel_frobenius(got, np.concatenate(ref, 0)) < TOL
+    assert_parity(got, np.concatenate(ref, 0))
 
 
 def test_mlp_hand_example_padded_bit_exact(tl, golden_dir):
@@ -346,7 +347,7 @@ def test_split_tail_items(tl, act):
     c.ag_gemm(cuda(A[0]), cuda(Bs[0]), C, act=act)
     torch.cuda.synchronize()
     _, Y = O.ag_gemm([TI.to_f64(A[0])], [TI.to_f64(Bs[0])])
-    assert O.rel_frobenius(f64(C), O.activation(Y[0], act)) < TOL
+    assert_parity(f64(C), O.activation(Y[0], act))
 
 
 # ----------------------------------------------------------------------------- copy-engine AG binding (NEXT-1)
@@ -368,7 +369,7 @@ def test_ag_dma_binding_parity(tl, W, act):
     _, Y = O.ag_gemm([TI.to_f64(a) for a in As], [TI.to_f64(b) for b in Bs])
     for r in range(W):
         assert torch.equal(Ag[r].cpu().view(torch.int16), full.view(torch.int16))
-        assert O.rel_frobenius(f64(Cs[r]), O.activation(Y[r], act)) < TOL
+        assert_parity(f64(Cs[r]), O.activation(Y[r], act))
 
 
 def test_ag_dma_binding_matches_sm_binding_and_epochs(tl):
@@ -405,17 +406,20 @@ def test_ag_dma_dropped_notify_times_out(tl):
 
 
 # ----------------------------------------------------------------------------- full-size sampled parity
-@pytest.mark.parametrize("name,M,H,I,W", [
-    ("llama7b", 8192, 4096, 11008, 1),      # bench.py's N=1 workload and launch configuration
-    ("llama7b", 8192, 4096, 11008, 8),      # BASELINE configs[1] (8 ranks, loopback on one GPU)
-    ("llama70b", 8192, 8192, 28672, 2),     # configs[2] at W=2
-    ("mixtral", 16384, 4096, 14336, 4),     # configs[3] at W=4
+@pytest.mark.parametrize("name,M,H,I,W,block", [
+    ("llama70b", 8192, 8192, 28672, 1, 0),    # bench.py's default N=1 workload and launch configuration
+    ("llama7b", 8192, 4096, 11008, 1, 0),
+    ("llama7b", 8192, 4096, 11008, 8, 3),     # BASELINE configs[1] (8 ranks, loopback): rank 3's whole block
+    ("llama70b", 8192, 8192, 28672, 2, None),  # configs[2] at W=2
+    ("mixtral", 16384, 4096, 14336, 4, None),  # configs[3] at W=4
 ])
-def test_full_size_sampled_rows(tl, name, M, H, I, W):
+def test_full_size_sampled_rows(tl, name, M, H, I, W, block):
     """Full BASELINE.json sizes; the oracle is evaluated exactly on sampled rows (rows are
-    independent), spread over every rank's output block."""
+    independent): rows spread over every rank's output block, the first 128-row tile, and (block =
+    rank index) one rank's whole output block -- every tile of it checked element-wise."""
     X, G, U, W2 = TI.mlp_full(M, H, I, seed=0)
     Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    del X, G, U, W2
     Mr = M // W
     outs = [empty(Mr, H) for _ in range(W)]
     if W == 1:
@@ -427,11 +431,17 @@ def test_full_size_sampled_rows(tl, name, M, H, I, W):
         c.mlp_forward_lb([cuda(x) for x in Xs], [cuda(w) for w in W1s], [cuda(w) for w in W2s], outs,
                          act=TI.ACT_SILU_MUL)
         assert c.check()[0] == 0
-    rows = sorted({r * Mr + o for r in range(W) for o in (0, Mr // 2, Mr - 1)} | {M // 3, 2 * M // 3})
+    rows = {r * Mr + o for r in range(W) for o in (0, Mr // 2, Mr - 1)} | {M // 3, 2 * M // 3} | set(range(128))
+    if block is not None:
+        rows |= set(range(block * Mr, (block + 1) * Mr))
+    rows = sorted(rows)
     ref = O.mlp_forward_rows([TI.to_f64(t) for t in Xs], [TI.to_f64(t) for t in W1s], [TI.to_f64(t) for t in W2s],
                              TI.ACT_SILU_MUL, rows)
-    got = np.stack([outs[i // Mr][i % Mr].float().cpu().double().numpy() for i in rows])
-    assert O.rel_frobenius(got, np.stack([ref[i] for i in rows])) < TOL
+    full = torch.cat(outs).float().cpu().double().numpy()
+    assert_parity(full[rows], np.stack([ref[i] for i in rows]))
+    if block is not None:   # the whole block again on its own, tiles aligned to the block
+        b = list(range(block * Mr, (block + 1) * Mr))
+        assert_parity(full[b], np.stack([ref[i] for i in b]))
     del c
 
 
@@ -453,7 +463,7 @@ def test_mlp_odd_worlds(tl, W, ring):
     assert st == 0, diag
     ref = O.mlp_forward([TI.to_f64(x) for x in Xs], [TI.to_f64(w) for w in W1s], [TI.to_f64(w) for w in W2s],
                         TI.ACT_SILU_MUL)
-    assert O.rel_frobenius(np.concatenate([f64(o) for o in outs], 0), np.concatenate(ref, 0)) < TOL
+    assert_parity(np.concatenate([f64(o) for o in outs], 0), np.concatenate(ref, 0))
 
 
 @pytest.mark.parametrize("opts", [
@@ -479,7 +489,7 @@ def test_mlp_option_matrix(tl, opts):
     assert st == 0, diag
     ref = O.mlp_forward([TI.to_f64(x) for x in Xs], [TI.to_f64(w) for w in W1s], [TI.to_f64(w) for w in W2s],
                         TI.ACT_SILU_MUL)
-    assert O.rel_frobenius(np.concatenate([f64(o) for o in outs], 0), np.concatenate(ref, 0)) < TOL
+    assert_parity(np.concatenate([f64(o) for o in outs], 0), np.concatenate(ref, 0))
 
 
 def test_small_m_many_ranks(tl):
@@ -494,7 +504,7 @@ def test_small_m_many_ranks(tl):
     assert c.check()[0] == 0
     ref = O.mlp_forward([TI.to_f64(x) for x in Xs], [TI.to_f64(w) for w in W1s], [TI.to_f64(w) for w in W2s],
                         TI.ACT_SILU_MUL)
-    assert O.rel_frobenius(np.concatenate([f64(o) for o in outs], 0), np.concatenate(ref, 0)) < TOL
+    assert_parity(np.concatenate([f64(o) for o in outs], 0), np.concatenate(ref, 0))
 
 
 def test_binding_shape_and_dtype_checks(tl):
@@ -539,7 +549,7 @@ def test_rs_dma_binding_matches_sm_binding(tl, W):
             assert torch.equal(outs[r], ref[r]), f"call {i} rank {r}"
     oracle = O.gemm_rs([TI.to_f64(x) for x in As], [TI.to_f64(x) for x in Bs])
     got = np.concatenate([f64(o) for o in ref], 0)
-    assert O.rel_frobenius(got, np.concatenate(oracle, 0)) < TOL
+    assert_parity(got, np.concatenate(oracle, 0))
 
 
 def test_mlp_both_dma_bindings(tl):
@@ -583,3 +593,17 @@ def test_rs_dma_binding_many_items_per_cta(tl, W, M, N):
         assert st == 0, diag
         for r in range(W):
             assert torch.equal(outs[r], ref[r])
+
+
+def test_debug_options_not_read_from_env(tl, monkeypatch):
+    """The fault-injection / debug switches change results on purpose, so the environment cannot turn
+    them on (only tl_set_option can); the tunables are still read from TL_<KEY>."""
+    monkeypatch.setenv("TL_DEBUG_MODE", "3")
+    monkeypatch.setenv("TL_DEBUG_DELAY_NS", "1000")
+    monkeypatch.setenv("TL_DEBUG_DROP_NOTIFY", "0")
+    monkeypatch.setenv("TL_COMM_TILE_ROWS", "128")
+    c = tl.Comm.single(0, max_M=256, max_H=128)
+    assert c.get_option("debug_mode") == 0 and c.get_option("debug_delay_ns") == 0
+    assert c.get_option("debug_drop_notify") == -1
+    assert c.get_option("comm_tile_rows") == 128
+    c.close()
