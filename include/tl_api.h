@@ -118,6 +118,11 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *   "debug_drop_rank"  see above
  *   "ag_binding"       AllGather resource binding: 0 = SMs (bulk-copy warp in every CTA),
  *                      1 = copy engines (cudaMemcpyAsync + stream write-value flags)
+ *   "ag_mode"          AllGather data-transfer mode: 0 = push (tile_push_data: each
+ *                      source's copy role writes its producer tiles into every rank's gathered buffer),
+ *                      1 = pull (tile_pull_data: each rank's copy role reads every source's tiles from
+ *                      that source's gathered buffer into its own, after the source's own copy of the
+ *                      tile is released).  Bitwise-identical results.  SM binding only (ag_binding = 0).
  *   "dma_tile_rows"    producer-tile rows for ag_binding = 1 (default 0 = M/world/4, >= 64)
  *   "rs_binding"       ReduceScatter resource binding: 0 = SMs (epilogue TMA-stores partial tiles into the
  *                      owners' slots), 1 = the paper's hybrid: partial tiles to a local outbox,

@@ -154,7 +154,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 0, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0;
+          n_sub = 0, ag_binding = 0, ag_mode = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0;
 };
 
 struct OptDesc {
@@ -175,6 +175,7 @@ const OptDesc kOpts[] = {
     {"debug_drop_rank", &Options::debug_drop_rank, -1, kMaxWorld - 1},
     {"n_sub", &Options::n_sub, 0, 2},
     {"ag_binding", &Options::ag_binding, 0, 1},
+    {"ag_mode", &Options::ag_mode, 0, 1},
     {"dma_tile_rows", &Options::dma_tile_rows, 0, 1 << 20},
     {"debug_mode", &Options::debug_mode, 0, 3},
     {"attn_poly", &Options::attn_poly, 0, 8},
@@ -520,6 +521,8 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   }
   const int64_t M_r = M / W;
   const bool dma = W > 1 && c->opt.ag_binding == 1;
+  if (dma && c->opt.ag_mode == AG_PULL)
+    return fail(TL_ERR_UNSUPPORTED, "ag_mode = 1 (pull) runs on the SM copy role; not with ag_binding = 1");
   int64_t tm = c->opt.comm_tile_rows;
   if (dma)  // copy-engine binding: few large copies (each costs a host call), default 4 per rank
     tm = c->opt.dma_tile_rows > 0 ? c->opt.dma_tile_rows : std::max<int64_t>(64, (M_r / 4 + 7) / 8 * 8);
@@ -572,6 +575,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   p.tiles_per_channel = sm.tiles_per_channel;
   p.copy_ctas = c->opt.copy_ctas > 0 ? (int)std::min<int64_t>(c->opt.copy_ctas, p.ctas_per_rank) : p.ctas_per_rank;
   p.row_bytes = (int)(K * 2);
+  p.ag_mode = (int)c->opt.ag_mode;
   p.rs_mode = RS_NONE;
   if (comm) {
     p.order = (M_r % (128 * pair) == 0) ? ORDER_AG_INTERLEAVE : ORDER_ROTATE;
@@ -1402,6 +1406,8 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
   // copy-engine binding: larger producer tiles (option dma_tile_rows, default S/world/4) so the host
   // enqueues few large copies; SM binding: comm_tile_rows
   const bool dma_bind = W > 1 && c->opt.ag_binding == 1;
+  if (dma_bind && c->opt.ag_mode == AG_PULL)
+    return fail(TL_ERR_UNSUPPORTED, "ag_mode = 1 (pull) runs on the SM copy role; not with ag_binding = 1");
   const int64_t tm = dma_bind ? (c->opt.dma_tile_rows > 0 ? c->opt.dma_tile_rows : std::max<int64_t>(64, S_r / 4))
                               : c->opt.comm_tile_rows;
   StaticMap sm = StaticMap::make((int)S, W, (int)std::max<int64_t>(1, std::min<int64_t>(tm, S_r)),
@@ -1442,6 +1448,7 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
   p.debug_mode = (c->opt.debug_mode == 1 || c->opt.debug_mode == 2) ? (int)c->opt.debug_mode : 0;
   if (p.debug_mode == 1) p.copy_ctas = 0;   // computation only: no K/V AllGather traffic
   p.row_bytes = (int)row_bytes;
+  p.ag_mode = (int)c->opt.ag_mode;
   const size_t kv_bytes = (size_t)S * row_bytes;
   // ag_binding = 1: the K/V AllGather on the copy engines (the paper's binding for this workload,
   // P:474 "uses host-side primitives ... copy engine"), leaving every SM to the attention

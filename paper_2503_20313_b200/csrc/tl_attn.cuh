@@ -66,6 +66,7 @@ struct alignas(64) AttnParams {
   uint32_t epoch;
   int tm_rows, tiles_per_rank, tiles_per_channel, copy_ctas, row_bytes;
   int drop_rank, drop_index;
+  int ag_mode;                      // 0 = push, 1 = pull (tl_params.h AgMode)
   uint32_t delay_ns, delay_seed;   // schedule perturbation (debug_delay, 0 = off)
   int debug_mode;                  // overlap ratio: 1 computation only, 2 communication only
 };
@@ -458,13 +459,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
         const int W = p.world;
         const int n_tasks = p.tiles_per_rank * W;
         for (int task = cta; task < n_tasks; task += p.copy_ctas) {
+          // push: (tile t, destination d); pull: (tile t of source d, into this rank's K/V banks), as in
+          // the GEMM kernel's copy role (tl_kernel.cuh)
           const int t = task / W, d = (rank + task % W) % W;
+          const bool pull = p.ag_mode == 1;
           debug_delay(p.delay_ns, p.delay_seed, rank, 2 * task);
           const int lo = t * p.tm_rows, hi = min(lo + p.tm_rows, p.S_r);
           const uint32_t bytes = (uint32_t)(hi - lo) * (uint32_t)p.row_bytes;
+          const int owner = pull ? d : rank, tgt = pull ? rank : d;
+          if (pull && d != rank)
+            tile_wait(p.ag_flags[d] + d * kAgFlagStride + t, p.epoch, p.timeout_ns, p.diag, rank, 1, d, t);
           for (int kv = 0; kv < 2; ++kv) {
-            const uint8_t* src = (kv ? ra.v_shard : ra.k_shard) + (size_t)lo * p.row_bytes;
-            uint8_t* dst = (kv ? p.vfull[d] : p.kfull[d]) + ((size_t)rank * p.S_r + lo) * p.row_bytes;
+            const size_t off = ((size_t)owner * p.S_r + lo) * p.row_bytes;
+            const uint8_t* src = (!pull || d == rank) ? (kv ? ra.v_shard : ra.k_shard) + (size_t)lo * p.row_bytes
+                                                      : (kv ? p.vfull[d] : p.kfull[d]) + off;
+            uint8_t* dst = (kv ? p.vfull[tgt] : p.kfull[tgt]) + off;
             const int n = (int)((bytes + 16383) / 16384);
             for (int i = 0; i < n; ++i) {
               const int bb = (g + i) & 1;
@@ -487,8 +496,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
             g += n;
             ptx::bulk_wait<0>();
           }
-          const bool drop = rank == p.drop_rank && t == p.drop_index && d == (rank + 1) % W;
-          if (!drop) tile_notify(p.ag_flags[d] + rank * kAgFlagStride + t, p.epoch);
+          const bool drop = rank == p.drop_rank && t == p.drop_index && d == (pull ? rank : (rank + 1) % W);
+          if (!drop) tile_notify(pull ? p.ag_flags[rank] + d * kAgFlagStride + t : p.ag_flags[d] + rank * kAgFlagStride + t,
+                                 p.epoch);
         }
       }
     }

@@ -471,13 +471,20 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         const int W = p.world;
         const int n_tasks = p.tiles_per_rank * W;
         for (int task = cta_in_rank; task < n_tasks; task += p.copy_ctas) {
-          const int t = task / W, d = (rank + task % W) % W;  // tile-major, self first, then r+1, ...
+          // tile-major, self first, then r+1, ...: push -> (tile t of this rank, destination d);
+          // pull -> (tile t of source s = d, into this rank's X_full)
+          const int t = task / W, d = (rank + task % W) % W;
+          const bool pull = p.ag_mode == AG_PULL;
           debug_delay(p.delay_ns, p.delay_seed, rank, 2 * task);
-          trace_ev(p.trace, TU_COPY, TK_COPY_START, rank, t, d);
           const int lo = t * p.tm_rows, hi = min(lo + p.tm_rows, p.M_r);
           const uint32_t bytes = (uint32_t)(hi - lo) * (uint32_t)p.row_bytes;
-          const uint8_t* src = ra.a_shard + (size_t)lo * p.row_bytes;
-          uint8_t* dst = p.xfull[d] + ((size_t)rank * p.M_r + lo) * p.row_bytes;
+          const int owner = pull ? d : rank;                 // rank whose rows this tile holds
+          const uint8_t* src = (!pull || d == rank) ? ra.a_shard + (size_t)lo * p.row_bytes
+                                                    : p.xfull[d] + ((size_t)d * p.M_r + lo) * p.row_bytes;
+          uint8_t* dst = p.xfull[pull ? rank : d] + ((size_t)owner * p.M_r + lo) * p.row_bytes;
+          if (pull && d != rank)   // tile_pull_data waits for the source's own copy of tile t (its self task)
+            tile_wait(p.ag_flags[d] + d * kAgFlagStride + t, p.epoch, p.timeout_ns, p.diag, rank, 1, d, t);
+          trace_ev(p.trace, TU_COPY, TK_COPY_START, rank, t, d);
           const int n = (int)((bytes + kCopyPiece - 1) / kCopyPiece);
           for (int i = 0; i < n; ++i) {
             const int b = (g + i) & 1;
@@ -498,10 +505,13 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
             ptx::bulk_commit();
           }
           g += n;
-          ptx::bulk_wait<0>();  // every byte of this producer tile has landed at rank d
+          ptx::bulk_wait<0>();  // every byte of this producer tile has landed (at rank d / here)
           trace_ev(p.trace, TU_COPY, TK_COPY_END, rank, t, d);
-          const bool drop = rank == p.drop_rank && t == p.drop_index && d == (rank + 1) % W;
-          if (!drop) tile_notify(p.ag_flags[d] + rank * kAgFlagStride + t, p.epoch);
+          // fault injection: the producer rank drop_rank skips one notify of tile drop_index (push: the
+          // one to rank r+1; pull: its own, which every puller and its own consumers wait on)
+          const bool drop = rank == p.drop_rank && t == p.drop_index && d == (pull ? rank : (rank + 1) % W);
+          if (!drop) tile_notify(pull ? p.ag_flags[rank] + d * kAgFlagStride + t : p.ag_flags[d] + rank * kAgFlagStride + t,
+                                 p.epoch);
           trace_ev(p.trace, TU_COPY, TK_NOTIFY, rank, t, d);
         }
       }

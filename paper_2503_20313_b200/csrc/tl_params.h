@@ -23,6 +23,11 @@ enum Order : int { ORDER_IDENTITY = 0, ORDER_AG_INTERLEAVE = 1, ORDER_ROTATE = 2
 // counter releases a flag, the copy engines move each finished block to the owner (host-enqueued
 // stream wait / memcpy / write-value), and the owner's epilogue reduces as in RS_ONESHOT.
 enum RsMode : int { RS_NONE = 0, RS_ONESHOT = 1, RS_RING = 2, RS_DMA = 3 };
+// AllGather data-transfer mode ("two modes for data transfer -- pull and push"):
+// push = the source's copy role writes each producer tile into every rank's X_full (tile_push_data);
+// pull = every rank's copy role reads the tile from the source's X_full into its own (tile_pull_data),
+// after the source has placed it there and released its own flag.
+enum AgMode : int { AG_PUSH = 0, AG_PULL = 1 };
 
 // Per rank driven by this launch (1 entry for a process-per-GPU comm, `world` for loopback).
 struct alignas(64) RankArgs {
@@ -60,6 +65,7 @@ struct alignas(64) Params {
   uint32_t epoch;
   // AG (producer = copy role, consumer = GEMM A loads)
   int tm_rows, tiles_per_rank, tiles_per_channel, copy_ctas, row_bytes;
+  int ag_mode;                      // AG_PUSH | AG_PULL
   // RS
   int rs_mode;
   int drop_rank, drop_index;

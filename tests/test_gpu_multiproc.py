@@ -87,7 +87,7 @@ def test_two_processes_ipc_mlp():
         assert all(np.array_equal(outs[0], o) for o in outs[1:])
 
 
-def _worker_all(rank, world, port, q, dma=False):
+def _worker_all(rank, world, port, q, mode="sm"):
     """One rank per process: the MLP layer, the MoE layer and SP attention through the
     process-group comm (IPC-mapped peers), results sent back for the oracle check."""
     import torch.distributed as dist
@@ -105,9 +105,11 @@ def _worker_all(rank, world, port, q, dma=False):
         comm = tl.Comm.from_process_group(None, 0, max_M=max(M, 512 * world), max_H=512, max_topk=2)
         comm.set_option("num_ctas", max(2, 148 // world // 2 * 2))
         comm.set_option("timeout_ms", 120000)
-        if dma:   # both exchanges on the copy engines (cross-process IPC copies + stream flags)
+        if mode == "dma":   # both exchanges on the copy engines (cross-process IPC copies + stream flags)
             comm.set_option("ag_binding", 1)
             comm.set_option("rs_binding", 1)
+        if mode == "pull":  # AllGathers in pull mode: each rank reads the peers' tiles from their buffers
+            comm.set_option("ag_mode", 1)
         out = torch.empty(M // world, H, device="cuda", dtype=torch.bfloat16)
         comm.mlp_forward(Xs[rank].cuda(), W1s[rank].cuda(), W2s[rank].cuda(), out, act=tl.ACT_SILU_MUL)
         res["mlp"] = out.float().cpu().numpy()
@@ -143,8 +145,8 @@ def _worker_all(rank, world, port, q, dma=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dma", [(2, False), (4, False), (2, True)])
-def test_processes_ipc_all_ops(world, dma):
+@pytest.mark.parametrize("world,mode", [(2, "sm"), (4, "sm"), (2, "dma"), (2, "pull"), (4, "pull")])
+def test_processes_ipc_all_ops(world, mode):
     """Every fused op over real processes (one rank each, CUDA IPC peers; the GPU is time-shared)."""
     import torch.multiprocessing as mp
     import tl_inputs as TI
@@ -152,7 +154,7 @@ def test_processes_ipc_all_ops(world, dma):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_all, args=(r, world, port, q, dma)) for r in range(world)]
+    procs = [ctx.Process(target=_worker_all, args=(r, world, port, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     got = {}
