@@ -1,5 +1,6 @@
 """The one-process-per-GPU path (tl_comm_create -> handle all-gather -> tl_comm_connect ->
-cudaIpcOpenMemHandle) exercised with 2 processes sharing the single test GPU.
+cudaIpcOpenMemHandle) exercised with real processes: one device per rank when the box has enough GPUs
+(the cross-device data plane over NVLink: tools/two_gpu_check.sh), else all ranks sharing cuda:0.
 
 Bootstrap runs over gloo (the NCCL path uses the same exchange code).  Each process drives one
 rank with half the SMs (num_ctas = 74), so the two persistent kernels can be co-resident when the
@@ -19,6 +20,13 @@ from parity import assert_parity
 pytestmark = pytest.mark.gpu
 
 
+def _device(rank, world):
+    """One GPU per rank when the box has enough (real NVLink peers: the cross-device data plane),
+    else every rank on cuda:0 (CUDA IPC within one device, half the SMs each)."""
+    n = torch.cuda.device_count()
+    return (rank, False) if n >= world else (0, True)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -32,14 +40,16 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        torch.cuda.set_device(0)
+        dev, shared = _device(rank, world)
+        torch.cuda.set_device(dev)
         import paper_2503_20313_b200 as tl
         import tl_inputs as TI
         M, H, I = 256, 128, 512
         X, G, U, W2 = TI.mlp_full(M, H, I, seed=4)
         Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, world, TI.ACT_SILU_MUL)
-        comm = tl.Comm.from_process_group(None, 0, max_M=M, max_H=H)
-        comm.set_option("num_ctas", 148 // world // 2 * 2)
+        comm = tl.Comm.from_process_group(None, dev, max_M=M, max_H=H)
+        if shared:
+            comm.set_option("num_ctas", 148 // world // 2 * 2)
         comm.set_option("timeout_ms", 60000)
         out = torch.empty(M // world, H, device="cuda", dtype=torch.bfloat16)
         res = []
@@ -94,7 +104,8 @@ def _worker_all(rank, world, port, q, mode="sm"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        torch.cuda.set_device(0)
+        dev, shared = _device(rank, world)
+        torch.cuda.set_device(dev)
         import paper_2503_20313_b200 as tl
         import tl_inputs as TI
         res = {}
@@ -102,8 +113,9 @@ def _worker_all(rank, world, port, q, mode="sm"):
         M, H, I = 128 * world, 128, 128 * world
         X, G, U, W2 = TI.mlp_full(M, H, I, seed=6)
         Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, world, TI.ACT_SILU_MUL)
-        comm = tl.Comm.from_process_group(None, 0, max_M=max(M, 512 * world), max_H=512, max_topk=2)
-        comm.set_option("num_ctas", max(2, 148 // world // 2 * 2))
+        comm = tl.Comm.from_process_group(None, dev, max_M=max(M, 512 * world), max_H=512, max_topk=2)
+        if shared:
+            comm.set_option("num_ctas", max(2, 148 // world // 2 * 2))
         comm.set_option("timeout_ms", 120000)
         if mode == "dma":   # both exchanges on the copy engines (cross-process IPC copies + stream flags)
             comm.set_option("ag_binding", 1)
@@ -145,9 +157,14 @@ def _worker_all(rank, world, port, q, mode="sm"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,mode", [(2, "sm"), (4, "sm"), (2, "dma"), (2, "pull"), (4, "pull")])
+@pytest.mark.parametrize("world,mode", [(2, "sm"), (4, "sm"), (2, "dma"), (2, "pull"), (4, "pull"), (8, "sm"),
+                                        (8, "pull"), (8, "dma")])
 def test_processes_ipc_all_ops(world, mode):
-    """Every fused op over real processes (one rank each, CUDA IPC peers; the GPU is time-shared)."""
+    """Every fused op over real processes (one rank each, CUDA IPC peers): one GPU per rank when the box
+    has them (NVLink peer stores / loads, TMA tensor stores into peer-mapped staging, sys-scope flags
+    across devices), else the one GPU time-shared (world 8 only runs with 8 devices)."""
+    if world > 4 and torch.cuda.device_count() < world:
+        pytest.skip(f"world {world} needs {world} devices (cross-device data-plane check)")
     import torch.multiprocessing as mp
     import tl_inputs as TI
     from oracle import tl_oracle as O

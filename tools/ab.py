@@ -38,7 +38,7 @@ def main():
     comms = []
     for cfg in cfgs:
         c = tl.Comm.single(0, max_M=M, max_H=H)
-        for kv in filter(None, cfg.split(",")):
+        for kv in filter(None, cfg.split(",") if cfg != "cublas" else []):
             k, v = kv.split("=")
             c.set_option(k, int(v))
         comms.append(c)
@@ -57,9 +57,24 @@ def main():
         if op in ("g2", "layer"):
             c.gemm_rs(Z, w2, out)
 
+    import threading
+    import time
     import pynvml
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    samples = []          # (t, watts, sm MHz) every ~10 ms (the energy counter is too coarse here)
+    stop = [False]
+
+    def sampler():
+        while not stop[0]:
+            try:
+                samples.append((time.perf_counter(), pynvml.nvmlDeviceGetPowerUsage(h) / 1e3,
+                                pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+            except Exception:
+                pass
+            time.sleep(0.01)
+    th = threading.Thread(target=sampler, daemon=True)
+    th.start()
     rounds, iters = int(os.environ.get("AB_ROUNDS", "6")), int(os.environ.get("AB_ITERS", "20"))
     for ci in range(len(cfgs)):
         for _ in range(3):
@@ -70,17 +85,21 @@ def main():
         order = list(range(len(cfgs))) if r % 2 == 0 else list(reversed(range(len(cfgs))))
         for ci in order:
             torch.cuda.synchronize()
-            e0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
+            t0 = time.perf_counter()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             for _ in range(iters):
                 run(ci)
             b.record()
             torch.cuda.synchronize()
-            e1 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
-            res[ci]["ms"].append(a.elapsed_time(b) / iters)
-            res[ci]["mj"].append((e1 - e0) / iters)
-            res[ci]["mhz"].append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            t1 = time.perf_counter()
+            ms = a.elapsed_time(b) / iters
+            win = [s for s in samples if t0 + 0.2 * (t1 - t0) <= s[0] <= t1]   # skip the ramp
+            pw = statistics.mean(s[1] for s in win) if win else float("nan")
+            res[ci]["ms"].append(ms)
+            res[ci]["mj"].append(pw * ms)             # W x ms = mJ
+            res[ci]["mhz"].append(statistics.median(s[2] for s in win) if win else float("nan"))
+    stop[0] = True
     for ci, cfg in enumerate(cfgs):
         ms = statistics.median(res[ci]["ms"])
         mj = statistics.median(res[ci]["mj"])
