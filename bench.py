@@ -357,9 +357,10 @@ def run_layer(args, ctx, M, emit=True):
     if x.numel() * 2 + w1.numel() * 2 + w2.numel() * 2 <= 126e6:   # small shapes: flush L2 between steps
         flush = torch.empty(128 * 2 ** 20, device="cuda", dtype=torch.int16)
 
-    def step():
-        comm.ag_gemm(x, w1, Z, act=act, stream=stream)   # kernel 1: AG + GEMM1 (+ SiLU*up)
-        comm.gemm_rs(Z, w2, out, stream=stream)          # kernel 2: GEMM2 + RS
+    fused = bool(comm.get_option("mlp_fused"))
+
+    def step():   # tl_mlp_forward: one fused launch (AG + GEMM1 + SiLU*up, then GEMM2 + RS)
+        comm.mlp_forward(x, w1, w2, out, act=act, Z=Z, stream=stream)
 
     def barrier():
         if distributed:
@@ -374,8 +375,8 @@ def run_layer(args, ctx, M, emit=True):
         step()
     barrier()
 
-    # ---- timed region: K steps, per-kernel CUDA events on the launching stream
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    # ---- timed region: K steps, CUDA events around each layer launch on the launching stream
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     barrier()
     nv0 = nvl.read()
     t_start = torch.cuda.Event(enable_timing=True)
@@ -385,10 +386,8 @@ def run_layer(args, ctx, M, emit=True):
         if flush is not None:
             flush.fill_(i)
         ev[i][0].record(stream)
-        comm.ag_gemm(x, w1, Z, act=act, stream=stream)
+        comm.mlp_forward(x, w1, w2, out, act=act, Z=Z, stream=stream)
         ev[i][1].record(stream)
-        comm.gemm_rs(Z, w2, out, stream=stream)
-        ev[i][2].record(stream)
     t_end.record(stream)
     barrier()
     nv1 = nvl.read()
@@ -398,21 +397,40 @@ def run_layer(args, ctx, M, emit=True):
             step()
         torch.cuda.synchronize()
     clk = clocks.stop()
-    k1 = [e[0].elapsed_time(e[1]) for e in ev]
-    k2 = [e[1].elapsed_time(e[2]) for e in ev]
-    k1_ms = max_over_ranks(sum(k1) / len(k1))
-    k2_ms = max_over_ranks(sum(k2) / len(k2))
+    lk = [e[0].elapsed_time(e[1]) for e in ev]
+    layer_ms = max_over_ranks(sum(lk) / len(lk))          # the layer's launch(es), mean per step
     if flush is None:
         total_ms = max_over_ranks(t_start.elapsed_time(t_end))
         ms = total_ms / args.steps
     else:   # the L2 flush between steps is not part of the layer
-        ms = k1_ms + k2_ms
+        ms = layer_ms
     st, diag = comm.check()
+    # breakdown (context, not the headline): the same layer as two launches, each timed on its own
+    comm.set_option("mlp_fused", 0)
+    for _ in range(2):
+        comm.ag_gemm(x, w1, Z, act=act, stream=stream)
+        comm.gemm_rs(Z, w2, out, stream=stream)
+    barrier()
+    bk = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for i in range(args.steps):
+        if flush is not None:
+            flush.fill_(i)
+        bk[i][0].record(stream)
+        comm.ag_gemm(x, w1, Z, act=act, stream=stream)
+        bk[i][1].record(stream)
+        comm.gemm_rs(Z, w2, out, stream=stream)
+        bk[i][2].record(stream)
+    barrier()
+    comm.set_option("mlp_fused", int(fused))
+    k1_ms = max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in bk) / args.steps)
+    k2_ms = max_over_ranks(sum(e[1].elapsed_time(e[2]) for e in bk) / args.steps)
+    comm.mlp_forward(x, w1, w2, out, act=act, Z=Z, stream=stream)   # `out` from the product path again
+    barrier()
     f1, f2 = layer_flops(M, H, I, Wl, gated)
     n_rank_units = 1 if args.rank_shape_of else W
     value = (f1 + f2) * n_rank_units / (ms * 1e-3) / 1e12        # whole job (all ranks), TFLOPS
     per_gpu = value / W
-    ach1 = f1 / (k1_ms * 1e-3) / 1e12
+    ach = (f1 + f2) / (layer_ms * 1e-3) / 1e12            # the fused kernel's FLOPs per launch / its time
     v_ag, v_rs = nvlink_bytes(M, H, W) if not args.rank_shape_of else (0, 0)
     # roofline: layer = max((F1+F2)/P_TC, (V_AG+V_RS)/B_NVL); two-phase form beside it
     t_tc = (f1 + f2) / (P_burst * 1e12)
@@ -420,7 +438,6 @@ def run_layer(args, ctx, M, emit=True):
     t_layer = max(t_tc, t_nvl)
     t_two = max(f1 / (P_burst * 1e12), v_ag / (B_NVL_MEASURED * 1e9)) + \
         max(f2 / (P_burst * 1e12), v_rs / (B_NVL_MEASURED * 1e9))
-    t_k1 = max(f1 / (P_burst * 1e12), v_ag / (B_NVL_MEASURED * 1e9))
     nvl_d = NvlinkCounters.delta(nv0, nv1)
     nvl_line = {"unavailable": nvl.why or "counters not exposed"} if nvl_d is None else {
         "source": nvl_d[0], "tx_bytes_per_step": nvl_d[1] / args.steps, "rx_bytes_per_step": nvl_d[2] / args.steps,
@@ -554,21 +571,25 @@ def run_layer(args, ctx, M, emit=True):
         "config": cfg,
         "options": opts,
         "tflops_per_gpu": round(per_gpu, 2),
-        "kernels_ms": {"ag_gemm_act": round(k1_ms, 4), "gemm_rs": round(k2_ms, 4)},
-        "roofline": {"bound": "tensor" if f1 / (P_burst * 1e12) >= v_ag / (B_NVL_MEASURED * 1e9) else "nvlink",
-                     "kernel": "tl_gemm_kernel (AG-GEMM1 + SiLU*up)", "achieved": round(ach1, 2),
-                     "peak": P_burst, "unit": "TFLOP/s", "frac": round(ach1 / P_burst, 4),
-                     "frac_sustained": round(ach1 / P_sust, 4), "peak_sustained": P_sust, "peak_source": peak_src,
-                     "kernel_roof_ms": round(t_k1 * 1e3, 4), "kernel_frac": round(t_k1 * 1e3 / k1_ms, 4),
+        "kernels_ms": {"mlp_fused" if fused else "ag_gemm_act+gemm_rs": round(layer_ms, 4),
+                       "unfused_breakdown": {"ag_gemm_act": round(k1_ms, 4), "gemm_rs": round(k2_ms, 4),
+                                             "sum": round(k1_ms + k2_ms, 4)}},
+        "roofline": {"bound": "tensor" if t_tc >= t_nvl else "nvlink",
+                     "kernel": ("tl_mlp_kernel (fused layer: AG + GEMM1 + SiLU*up, then GEMM2 + RS)" if fused else
+                                "tl_gemm_kernel x2 (AG-GEMM1 + SiLU*up; GEMM2 + RS)"),
+                     "achieved": round(ach, 2),
+                     "peak": P_burst, "unit": "TFLOP/s", "frac": round(ach / P_burst, 4),
+                     "frac_sustained": round(ach / P_sust, 4), "peak_sustained": P_sust, "peak_source": peak_src,
+                     "kernel_roof_ms": round(t_layer * 1e3, 4), "kernel_frac": round(t_layer * 1e3 / layer_ms, 4),
                      "layer_roof_ms": round(t_layer * 1e3, 4), "layer_frac": round(t_layer * 1e3 / ms, 4),
                      "layer_roof_terms_ms": {"tensor": round(t_tc * 1e3, 4), "nvlink": round(t_nvl * 1e3, 4)},
                      "two_phase_roof_ms": round(t_two * 1e3, 4), "two_phase_frac": round(t_two * 1e3 / ms, 4),
                      "nvlink_GBps_per_dir": B_NVL_MEASURED, "nvlink_bytes_per_dir": {"ag": v_ag, "rs": v_rs},
-                     "traffic": None, "per_launch_flop": f1},
+                     "traffic": None, "per_launch_flop": f1 + f2},
         "nvlink_counters": dict(nvl_line, max_tx_bytes_per_step_over_ranks=nvl_tx) if W > 1 else None,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (1 if fused else 2) * args.steps,
         "clocks": clk,
         "parity": parity,
         "baseline_nccl_cublas": base,

@@ -154,7 +154,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 0, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, ag_mode = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0;
+          n_sub = 0, ag_binding = 0, ag_mode = 0, mlp_fused = 1, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0;
 };
 
 struct OptDesc {
@@ -176,6 +176,7 @@ const OptDesc kOpts[] = {
     {"n_sub", &Options::n_sub, 0, 2},
     {"ag_binding", &Options::ag_binding, 0, 1},
     {"ag_mode", &Options::ag_mode, 0, 1},
+    {"mlp_fused", &Options::mlp_fused, 0, 1},
     {"dma_tile_rows", &Options::dma_tile_rows, 0, 1 << 20},
     {"debug_mode", &Options::debug_mode, 0, 3},
     {"attn_poly", &Options::attn_poly, 0, 8},
@@ -215,6 +216,11 @@ struct tl_comm {
   size_t rs_outbox_bytes[kMaxWorld] = {};
   uint32_t* rs_dma_sync[kMaxWorld] = {};    // [2][world][kRsFlagStride]: chunk counters, ready flags            // routing-table kernel: per-CTA counts + grid-barrier counter
   unsigned moe_tab_calls[kMaxWorld] = {};   // routing-table calls so far (2 barrier generations each)
+  // fused MLP kernel: per local rank Z-row counters (one per 256-row m-block), calls since the last reset
+  uint32_t* zdone[kMaxWorld] = {};
+  size_t zdone_n = 0;
+  uint32_t zdone_calls = 0;
+  int64_t zdone_M = -1, zdone_N = -1;
 };
 
 namespace {
@@ -354,6 +360,40 @@ tl_status launch(tl_comm* c, const Params& p, int epi, bool ag, int nsub, cudaSt
   return launch_t<1, EPI_RS, false, 1>(c, p, s);
 }
 
+template <int kEpi, bool kAG, int kNSub>
+tl_status launch_mlp_t(tl_comm* c, const Params& p1, const Params& p2, cudaStream_t stream) {
+  constexpr int kStages = stages_for(2, kAG, kNSub);
+  using L = Layout<2, kStages, kAG, kNSub>;
+  static_assert(2 * sizeof(Params) <= 32764, "two Params must fit the kernel parameter space");
+  auto kern = tl_mlp_kernel<2, kStages, kEpi, kAG, kNSub>;
+  TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::smem_request));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p1.n_local * p1.ctas_per_rank);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = L::smem_request;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = c->opt.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  TL_CUDA(cudaLaunchKernelEx(&cfg, kern, p1, p2));
+  return TL_OK;
+}
+
+tl_status launch_mlp(tl_comm* c, const Params& p1, const Params& p2, int act, bool ag, int nsub, cudaStream_t s) {
+  if (act == TL_ACT_SILU_MUL) {
+    if (nsub == 2) return ag ? launch_mlp_t<EPI_SILU_MUL, true, 2>(c, p1, p2, s) : launch_mlp_t<EPI_SILU_MUL, false, 2>(c, p1, p2, s);
+    return ag ? launch_mlp_t<EPI_SILU_MUL, true, 1>(c, p1, p2, s) : launch_mlp_t<EPI_SILU_MUL, false, 1>(c, p1, p2, s);
+  }
+  if (nsub == 2) return ag ? launch_mlp_t<EPI_STORE, true, 2>(c, p1, p2, s) : launch_mlp_t<EPI_STORE, false, 2>(c, p1, p2, s);
+  return ag ? launch_mlp_t<EPI_STORE, true, 1>(c, p1, p2, s) : launch_mlp_t<EPI_STORE, false, 1>(c, p1, p2, s);
+}
+
 // Split point of the work list: with 512-wide tiles a last wave that is at most half full is run
 // as 256-wide half items (half the time), every other tile whole.
 void set_items(Params& p, int nsub, int n_pairs) {
@@ -373,24 +413,32 @@ void set_items(Params& p, int nsub, int n_pairs) {
 // 256-wide tiles (TMEM double-buffered, epilogue hidden) cost 1.12 per k-block (extra L2->SMEM
 // traffic); 512-wide tiles cost 2 per k-block plus ~9 for the un-overlapped epilogue; half items
 // (split tail) cost 1 per k-block plus ~4.5.
+// Model time (in 256-wide k-block units) of the GEMM with 256-wide (nsub 1) and 512-wide (nsub 2) tiles.
+void nsub_costs(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gated, bool rs, double& t1, double& t2);
+
 int choose_nsub(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gated, bool rs = false) {
   if (pair_of(c) != 2) return 1;
   if (c->opt.n_sub == 1 || c->opt.n_sub == 2) return (int)c->opt.n_sub;
+  double t1, t2;
+  nsub_costs(c, M, N_out, K, gated, rs, t1, t2);
+  return t2 < t1 ? 2 : 1;
+}
+
+void nsub_costs(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gated, bool rs, double& t1, double& t2) {
   const int64_t P = ctas_per_rank(c) / 2;
   const int64_t m_blocks = (M + 255) / 256;
   const double kb = (double)((K + kBK - 1) / kBK);
   const int64_t bn1 = gated ? 128 : 256;
   const int64_t T1 = m_blocks * ((N_out + bn1 - 1) / bn1);
   const int64_t T2 = m_blocks * ((N_out + 2 * bn1 - 1) / (2 * bn1));
-  const double t1 = (double)((T1 + P - 1) / P) * 1.12 * kb;
+  t1 = (double)((T1 + P - 1) / P) * 1.12 * kb;
   const int64_t rem = T2 % P;
   // un-overlapped epilogue of a 512-wide tile: ~9 k-blocks for the gated (activation) and the
   // reduce-scatter epilogues, ~3.5 for a plain store (refit on the TP-2..8 rank shapes:
   // profiles/r01_nsub_ab.log, 512-wide 3-8 % faster where the old constant chose 256-wide)
   const double epi = (gated || rs) ? 9.0 : 3.5;
   const double full2 = 2.0 * kb + epi;
-  const double t2 = (double)(T2 / P) * full2 + (rem == 0 ? 0.0 : (2 * rem <= P ? kb + epi / 2 : full2));
-  return t2 < t1 ? 2 : 1;
+  t2 = (double)(T2 / P) * full2 + (rem == 0 ? 0.0 : (2 * rem <= P ? kb + epi / 2 : full2));
 }
 
 tl_status zero_fill(void* out, int64_t n, cudaStream_t s) {
@@ -489,9 +537,11 @@ tl_status dma_join(tl_comm* c, cudaStream_t stream) {
   return TL_OK;
 }
 
+// prep != nullptr: fill *prep with the launch parameters (tile width `nsub_force`) and do not launch (the
+// fused MLP kernel's phase 1; SM bindings only).
 tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, void* const* C,
                        void* const* Agath, int64_t M, int64_t N_out, int64_t K, int act, cudaStream_t stream,
-                       const MoeArgs* moe = nullptr) {
+                       const MoeArgs* moe = nullptr, int nsub_force = 0, Params* prep = nullptr) {
   tl_status st = check_comm(c);
   if (st != TL_OK) return st;
   const int W = c->world;
@@ -564,7 +614,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   // profiles/r01_moe_nsub_probe.log).
   const int nsub = moe ? ((pair_of(c) == 2 && c->opt.n_sub != 1 &&
                            (c->opt.n_sub == 2 || N_out > (act != TL_ACT_NONE ? 128 : 256))) ? 2 : 1)
-                       : choose_nsub(c, M, N_out, K, act != TL_ACT_NONE);
+                   : nsub_force ? nsub_force : choose_nsub(c, M, N_out, K, act != TL_ACT_NONE);
   const int bn_out = (act ? 128 : 256) * nsub;
   p.n_blocks = (int)((N_out + bn_out - 1) / bn_out);
   p.k_blocks = (int)((K + kBK - 1) / kBK);
@@ -679,6 +729,11 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
       p.rk[i].moe_sched = sched;
     }
   }
+  if (st == TL_OK && prep) {
+    *prep = p;
+    delete pp;
+    return TL_OK;
+  }
   if (st == TL_OK) {
     const int epi = act == TL_ACT_NONE ? EPI_STORE : act == TL_ACT_SILU_MUL ? EPI_SILU_MUL : EPI_GELU_MUL;
     st = moe ? launch_moe(c, p, epi, comm, nsub, stream) : launch(c, p, epi, comm, nsub, stream);
@@ -699,7 +754,7 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
 
 // ---------------------------------------------------------------- GEMM-RS
 tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, void* const* C, int64_t M, int64_t N,
-                       int64_t K, cudaStream_t stream) {
+                       int64_t K, cudaStream_t stream, int nsub_force = 0, Params* prep = nullptr) {
   tl_status st = check_comm(c);
   if (st != TL_OK) return st;
   const int W = c->world;
@@ -713,7 +768,7 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
   if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31)) return fail(TL_ERR_UNSUPPORTED, "dimension >= 2^31");
   const int64_t M_r = M / W;
   const int pair = pair_of(c);
-  const int nsub = choose_nsub(c, M, N, K, false, W > 1);
+  const int nsub = nsub_force ? nsub_force : choose_nsub(c, M, N, K, false, W > 1);
   const int64_t n_blocks = (N + 256 * nsub - 1) / (256 * nsub);
   if (W > 1) {
     if (M_r % 128) return fail(TL_ERR_UNSUPPORTED, "GEMM-RS with world > 1 needs (M/world) %% 128 == 0 (M/world=%lld)",
@@ -817,6 +872,11 @@ tl_status gemm_rs_impl(tl_comm* c, const void* const* A, const void* const* B, v
   // (CUDA_DEVICE_MAX_CONNECTIONS), and a wait-value queued ahead of the kernel that satisfies it would
   // deadlock.  The copy streams are ordered after the work that precedes the kernel (ev_start), never
   // after the kernel itself.
+  if (st == TL_OK && prep) {
+    *prep = p;
+    delete pp;
+    return TL_OK;
+  }
   if (st == TL_OK && dma) {
     st = dma_streams(c);
     if (st == TL_OK && cudaEventRecord(c->ev_start, stream) != cudaSuccess) st = fail(TL_ERR_CUDA, "event record");
@@ -891,9 +951,71 @@ tl_status mlp_impl(tl_comm* c, const void* const* X, const void* const* W1, cons
   if (H > c->max_H || M > c->max_M) return fail(TL_ERR_INVALID, "M/H exceed comm capacity");
   for (int i = 0; i < c->n_local; ++i)
     if (!out[i] || !aligned16(out[i]) || !W2[i] || !aligned16(W2[i])) return fail(TL_ERR_INVALID, "bad out/W2 pointer");
-  st = ag_gemm_impl(c, X, W1, z, nullptr, M, I_l, H, act, stream);
-  if (st != TL_OK) return st;
-  return gemm_rs_impl(c, z, W2, out, M, H, I_l, stream);
+  // One fused launch (phase 1 AG + GEMM1 + act, phase 2 GEMM2 + RS; tl_kernel.cuh tl_mlp_kernel) on the
+  // SM bindings; the copy-engine bindings, GeLU, single-SM tiles and the measurement debug modes run the
+  // two kernels.
+  const bool fused = c->opt.mlp_fused && pair_of(c) == 2 && act != TL_ACT_GELU_TANH_MUL && c->opt.ag_binding == 0 &&
+                     c->opt.rs_binding == 0 && c->opt.debug_mode == 0 && M > 0 && H > 0 && I_l > 0;
+  if (!fused) {
+    st = ag_gemm_impl(c, X, W1, z, nullptr, M, I_l, H, act, stream);
+    if (st != TL_OK) return st;
+    return gemm_rs_impl(c, z, W2, out, M, H, I_l, stream);
+  }
+  // one tile width for both phases: the one with the lower modelled sum
+  int nsub = (int)c->opt.n_sub;
+  if (nsub != 1 && nsub != 2) {
+    double a1, a2, b1, b2;
+    nsub_costs(c, M, I_l, H, act != TL_ACT_NONE, false, a1, a2);
+    nsub_costs(c, M, H, I_l, false, c->world > 1, b1, b2);
+    nsub = (a2 + b2 < a1 + b1) ? 2 : 1;
+  }
+  // validate both halves before either consumes an epoch
+  if (H % 8) return fail(TL_ERR_INVALID, "H must be a multiple of 8");
+  Params* pp = new Params[2];
+  st = ag_gemm_impl(c, X, W1, z, nullptr, M, I_l, H, act, stream, nullptr, nsub, &pp[0]);
+  if (st == TL_OK) st = gemm_rs_impl(c, z, W2, out, M, H, I_l, stream, nsub, &pp[1]);
+  if (st == TL_OK) {   // Z-row counters (local), reset when the shape changes
+    const size_t nblk = (size_t)((M + 255) / 256) + 1;
+    TL_CUDA(cudaSetDevice(c->device));
+    if (c->zdone_n < nblk) {
+      for (int i = 0; i < c->n_local; ++i) {
+        if (c->zdone[i]) {
+          cudaStreamSynchronize(stream);
+          cudaFree(c->zdone[i]);
+          c->zdone[i] = nullptr;
+        }
+        if (cudaMalloc(&c->zdone[i], nblk * sizeof(uint32_t)) != cudaSuccess) { st = fail(TL_ERR_CUDA, "zdone alloc"); break; }
+      }
+      c->zdone_n = st == TL_OK ? nblk : 0;
+      c->zdone_M = -1;
+    }
+    if (st == TL_OK && (c->zdone_M != M || c->zdone_N != I_l)) {
+      for (int i = 0; i < c->n_local && st == TL_OK; ++i)
+        if (cudaMemsetAsync(c->zdone[i], 0, c->zdone_n * sizeof(uint32_t), stream) != cudaSuccess)
+          st = fail(TL_ERR_CUDA, "zdone reset");
+      c->zdone_M = M;
+      c->zdone_N = I_l;
+      c->zdone_calls = 0;
+    }
+  }
+  if (st == TL_OK && c->world > 1 && (M / c->world) % 256 == 0) {
+    // phase 2 in phase 1's completion order (ORDER_RS_INTERLEAVE), raster groups of (W-1) x k m-blocks that
+    // never straddle the remote / own boundary (k | blocks per rank, (W-1) k <= 16)
+    const int W = c->world, bpr = (int)(M / W / 256);
+    int k = 1;
+    for (int d = 1; d <= bpr; ++d)
+      if (bpr % d == 0 && (W - 1) * d <= 16) k = d;
+    pp[1].order = ORDER_RS_INTERLEAVE;
+    pp[1].raster_group = (W - 1) * k;
+  }
+  if (st == TL_OK) {
+    ++c->zdone_calls;
+    for (int i = 0; i < c->n_local; ++i) pp[0].zdone[i] = pp[1].zdone[i] = c->zdone[i];
+    pp[1].zdone_target = c->zdone_calls * (uint32_t)(8 * I_l);
+    st = launch_mlp(c, pp[0], pp[1], act, c->world > 1, nsub, stream);
+  }
+  delete[] pp;
+  return st;
 }
 
 tl_status alloc_ws(tl_comm* c, int r) {
@@ -1058,6 +1180,8 @@ tl_status tl_comm_destroy(tl_comm_t c) {
     if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
   }
   if (c->ev_start) cudaEventDestroy(c->ev_start);
+  for (int i = 0; i < kMaxWorld; ++i)
+    if (c->zdone[i]) cudaFree(c->zdone[i]);
   for (int i = 0; i < kMaxWorld; ++i) {
     if (c->moe_buf[i]) cudaFree(c->moe_buf[i]);
     if (c->tab_sync[i]) cudaFree(c->tab_sync[i]);

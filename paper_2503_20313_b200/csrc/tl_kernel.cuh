@@ -67,6 +67,11 @@ __device__ __forceinline__ int m_perm(const Params& p, int rank, int m_rot, int 
     const int jj = j - bpr, loc = jj / (p.world - 1), s = (rank + 1 + jj % (p.world - 1)) % p.world;
     return s * bpr + loc;
   }
+  if (p.order == ORDER_RS_INTERLEAVE) {
+    const int bpr = p.m_blocks / p.world, R = (p.world - 1) * bpr;
+    if (j < R) return ((rank + 1 + j % (p.world - 1)) % p.world) * bpr + j / (p.world - 1);
+    return rank * bpr + (j - R);
+  }
   if (p.order == ORDER_ROTATE) return (j + m_rot) % p.m_blocks;
   return j;
 }
@@ -103,15 +108,20 @@ __device__ __forceinline__ void item_coords(const Params& p, int item, int& t, i
 // ragged N) computes only its first sub-tile: every role (producer, MMA, epilogue) applies the same
 // clamp, so loads, MMAs, stores and RS flags stay consistent.  (The 7B TP-8 GEMM1, N_out = 1376,
 // wasted half of its last n-block: ~8 % of the MMAs.)
-template <int kNSub, int kEpi, int kMoE>
-__device__ __forceinline__ void clamp_subs(const Params& p, int nb, int sub_lo, int& sub_n) {
-  // (not for the ReduceScatter: its per-sub-tile flags must match across ranks whose schedules split
-  // different tiles)
-  if constexpr (kNSub == 2 && kMoE == MOE_NONE && kEpi != EPI_RS) {
-    constexpr int sub_w = (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) ? 128 : 256;   // output columns
+// (not for the ReduceScatter: its per-sub-tile flags must match across ranks whose schedules split
+// different tiles).  `epi` = the epilogue of the item's GEMM (the fused MLP kernel runs two).
+template <int kNSub, int kMoE>
+__device__ __forceinline__ void clamp_subs(const Params& p, int nb, int sub_lo, int& sub_n, int epi) {
+  if constexpr (kNSub == 2 && kMoE == MOE_NONE) {
+    if (epi == EPI_RS) return;
+    const int sub_w = (epi == EPI_SILU_MUL || epi == EPI_GELU_MUL) ? 128 : 256;   // output columns
     if (sub_lo == 0 && sub_n == 2 && (nb * 2 + 1) * sub_w >= p.N_out) sub_n = 1;
   }
 }
+
+// Epilogue kind of phase 2 of the fused MLP kernel: the ReduceScatter epilogue across ranks, a plain store
+// at world 1.
+__device__ __forceinline__ int phase2_epi(const Params& p) { return p.rs_mode != RS_NONE ? EPI_RS : EPI_STORE; }
 
 // MoE work item -> (m-tile of the padded grouped rows, n-block, expert).  Tiles run in the order
 // of the device-built schedule (by the producer tile their last token needs, i.e. by expected
@@ -222,8 +232,14 @@ __device__ __forceinline__ void epi_load(uint32_t tacc, int pc, float* r) {
   }
 }
 
-template <int kPair, int kStages, int kEpi, bool kAG, int kNSub, int kMoE = MOE_NONE>
-__global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_constant__ Params p) {
+// The persistent CTA body.  kFused (tl_mlp_kernel): the whole MLP layer in one launch -- phase 1 items
+// (p1: AG + GEMM1 + activation -> Z) then phase 2 items (p2: GEMM2 + RS), one work list per CTA pair; a
+// phase-2 tile of m-block b waits (acquire, gpu scope) until every phase-1 tile of b has stored its Z
+// rows (per-m-block counters released by the epilogue warps), so GEMM2 starts on the first finished row
+// blocks while GEMM1's last wave still runs: one fill and one drain for the layer instead of two.
+template <int kPair, int kStages, int kEpi, bool kAG, int kNSub, int kMoE, bool kFused>
+__device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
+  const Params& p = p1;   // launch-wide parameters (phase 1); per-item code re-binds p to its phase
   using L = Layout<kPair, kStages, kAG, kNSub>;
   constexpr int kAccBufs = 2 / kNSub;          // TMEM accumulator buffers (512 columns in total)
   constexpr int kAccCols = kUmmaN * kNSub;
@@ -263,6 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     ptx::prefetch_tmap(&ra.tm_a);
     ptx::prefetch_tmap(&ra.tm_b0);
     if (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) ptx::prefetch_tmap(&ra.tm_b1);
+    if constexpr (kFused) {
+      ptx::prefetch_tmap(&p2.rk[lr].tm_a);
+      ptx::prefetch_tmap(&p2.rk[lr].tm_b0);
+    }
   }
   if (warp == 2) ptx::tmem_alloc<kPair>(tmem_slot, 512);
   ptx::tc_fence_before();
@@ -276,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // MoE: the number of m-tiles is data dependent (built on the device from the routing)
-  const int total = p.debug_mode == 2 ? 0 : kMoE ? ra.moe_tab[0] * p.n_blocks : p.n_items;
+  const int total = p.debug_mode == 2 ? 0 : kMoE ? ra.moe_tab[0] * p.n_blocks : p.n_items + (kFused ? p2.n_items : 0);
 
   // MoE producer: the 32 row gathers (tile::gather4) of every k-block are issued by two threads
   // (warp 0 lane 0: gathers 0-15 + the expert's B tile + the barrier arm; warp 2 lane 0: gathers
@@ -352,13 +372,33 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       int stage = 0;
       uint32_t phase = 0;
       for (int item = pair; item < total; item += n_pairs) {
+        const bool ph2 = kFused && item >= p1.n_items;
+        const Params& p = ph2 ? p2 : p1;
+        const RankArgs& ra = p.rk[lr];
+        const int itl = ph2 ? item - p1.n_items : item;
+        const int epi = ph2 ? phase2_epi(p) : kEpi;
+        const bool gated = epi == EPI_SILU_MUL || epi == EPI_GELU_MUL;
         int t, sub_lo, sub_n, mb, nb, expert = 0;
-        item_coords<kNSub>(p, item, t, sub_lo, sub_n);
+        item_coords<kNSub>(p, itl, t, sub_lo, sub_n);
         if constexpr (kMoE == MOE_SCATTER) moe_coords(p, ra, item, mb, nb, expert);
         else tile_coords(p, rank, ra.m_rot, t, mb, nb);
-        clamp_subs<kNSub, kEpi, kMoE>(p, nb, sub_lo, sub_n);
+        clamp_subs<kNSub, kMoE>(p, nb, sub_lo, sub_n, epi);
         const int row0 = mb * BM + cta_in_pair * 128;
-        if constexpr (kAG) {
+        if (ph2) {
+          // GEMM2 A rows = Z rows of m-block mb: wait until every GEMM1 tile of the block stored them
+          if (row0 < p.M) {
+            // monotone counter, compared modulo 2^32 (target = calls x 8 warps x N_out of GEMM1)
+            const unsigned* cnt = p.zdone[lr] + mb;
+            if ((int)(ptx::ld_acquire_gpu(cnt) - p.zdone_target) < 0) {
+              const uint64_t t0 = ptx::globaltimer();
+              while ((int)(ptx::ld_acquire_gpu(cnt) - p.zdone_target) < 0) {
+                __nanosleep(32);
+                if (ptx::globaltimer() - t0 > 20000000000ull) __trap();   // a lost Z tile is a bug, not a peer stall
+              }
+            }
+            ptx::fence_proxy_async_global();
+          }
+        } else if constexpr (kAG) {
           if (p.debug_mode != 1 && row0 < p.M) {
             debug_delay(p.delay_ns, p.delay_seed, rank, 2 * item + 1);
             if (cta_in_pair == 0) trace_ev(p.trace, TU_COMPUTE, TK_WAIT_START, rank, item);
@@ -388,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
 #pragma unroll
               for (int q = 0; q < NS; ++q) {
                 const int sub = s_lo + q;
-                if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL)
+                if (gated)
                   ptx::tma_load_2d_pair(cta_in_pair == 0 ? &ra.tm_b0 : &ra.tm_b1, &full[stage], sb + sub * L::kBBox,
                                         kc, nb * 128 * kNSub + sub * 128);
                 else
@@ -397,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
               }
             } else {
               ptx::tma_load_2d(&ra.tm_a, &full[stage], sa, kc, row0);
-              if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) {
+              if (gated) {
                 ptx::tma_load_2d(&ra.tm_b0, &full[stage], sb, kc, nb * 128);
                 ptx::tma_load_2d(&ra.tm_b1, &full[stage], sb + 128 * 128, kc, nb * 128);
               } else {
@@ -422,12 +462,18 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       int stage = 0, it = 0;
       uint32_t phase = 0;
       for (int item = pair; item < total; item += n_pairs, ++it) {
+        const bool ph2 = kFused && item >= p1.n_items;
+        const Params& p = ph2 ? p2 : p1;
+        const int itl = ph2 ? item - p1.n_items : item;
         int t, sub_lo, sub_n;
-        item_coords<kNSub>(p, item, t, sub_lo, sub_n);
-        if constexpr (kNSub == 2 && kMoE == MOE_NONE && kEpi != EPI_RS) {
-          int mb_, nb_;
-          tile_coords(p, rank, ra.m_rot, t, mb_, nb_);
-          clamp_subs<kNSub, kEpi, kMoE>(p, nb_, sub_lo, sub_n);
+        item_coords<kNSub>(p, itl, t, sub_lo, sub_n);
+        if constexpr (kNSub == 2 && kMoE == MOE_NONE) {
+          const int epi = ph2 ? phase2_epi(p) : kEpi;
+          if (epi != EPI_RS) {
+            int mb_, nb_;
+            tile_coords(p, rank, p.rk[lr].m_rot, t, mb_, nb_);
+            clamp_subs<kNSub, kMoE>(p, nb_, sub_lo, sub_n, epi);
+          }
         }
         const int as = it % kAccBufs;
         ptx::mbar_wait(&tempty[as], ((it / kAccBufs) & 1) ^ 1);
@@ -524,13 +570,21 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     int pf_item = -1;                        // MoE scatter: item whose scatter target was prefetched
     int4 pf_scat = make_int4(-1, 0, 0, 0);
     for (int item = pair; item < total; item += n_pairs, ++it) {
+      const bool ph2 = kFused && item >= p1.n_items;
+      const Params& p = ph2 ? p2 : p1;
+      const RankArgs& ra = p.rk[lr];
+      const int itl = ph2 ? item - p1.n_items : item;
+      const int epi = ph2 ? phase2_epi(p) : kEpi;
       int t, sub_lo, sub_n, mb, nb, expert;
-      item_coords<kNSub>(p, item, t, sub_lo, sub_n);
+      item_coords<kNSub>(p, itl, t, sub_lo, sub_n);
       if constexpr (kMoE == MOE_SCATTER) mb = moe_scatter_tile(p, ra, item, nb);
       else if constexpr (kMoE) moe_coords(p, ra, item, mb, nb, expert);
       else tile_coords(p, rank, ra.m_rot, t, mb, nb);
-      clamp_subs<kNSub, kEpi, kMoE>(p, nb, sub_lo, sub_n);
+      clamp_subs<kNSub, kMoE>(p, nb, sub_lo, sub_n, epi);
       (void)expert;
+      // the item's epilogue, instantiated per epilogue kind (the fused kernel runs two)
+      auto body = [&](auto e_c) {
+      constexpr int kE = decltype(e_c)::value;
       const int as = it % kAccBufs;
       ptx::mbar_wait(&tfull[as], (it / kAccBufs) & 1);
       ptx::tc_fence_after();
@@ -542,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         if (lane == 0) ptx::mbar_arrive_cluster(&tempty[as], 0);
       };
       // ---- per-tile action: plain/gated store, or (GEMM-RS) push to a peer slot / own reduce
-      constexpr bool kGated = (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL);
+      constexpr bool kGated = (kE == EPI_SILU_MUL || kE == EPI_GELU_MUL);
       constexpr int kPPS = kGated ? 4 : 8;                     // 32-column output pieces per sub-tile
       const int pc0 = sub_lo * kPPS, pc_end = (sub_lo + sub_n) * kPPS;
       constexpr int kPW = kGated ? 64 : 32;                   // fp32 registers per loaded piece
@@ -553,11 +607,11 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       int tgt = 0, slot = 0, tile = 0, myrow = 0;
       uint32_t add_mask = 0;                                   // slots to add (ascending rank order)
       const uint16_t* stg = nullptr;
-      if constexpr (kEpi == EPI_RS) {
+      if constexpr (kE == EPI_RS) {
         if (row0 >= p.M) {                                     // half-tile past the last row
           release_tmem();
           if (cta_in_pair == 0 && ew == 0 && lane == 0) trace_ev(p.trace, TU_COMPUTE, TK_TILE_END, rank, item);
-          continue;
+          return;
         }
         const int W = p.world;
         const int o = row0 / p.M_r;                 // owner of these rows (offset in the global view)
@@ -615,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
       // one item ahead: a single coalesced load whose latency overlaps the previous item's stores)
       uint16_t* moe_dst = nullptr;
       float moe_wt = 0.f;
-      if constexpr (kEpi == EPI_MOE_SCATTER) {
+      if constexpr (kE == EPI_MOE_SCATTER) {
         const int4 sc = (item == pf_item) ? pf_scat : ra.moe_scat[row0 + ew * 32 + (int)lane];
         if (sc.x >= 0) {
           moe_wt = __int_as_float(sc.z);
@@ -634,20 +688,20 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         if constexpr (kGated) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float a0 = (kEpi == EPI_SILU_MUL ? silu_f(r[2 * i]) : gelu_tanh_f(r[2 * i])) * r[32 + 2 * i];
+            const float a0 = (kE == EPI_SILU_MUL ? silu_f(r[2 * i]) : gelu_tanh_f(r[2 * i])) * r[32 + 2 * i];
             const float a1 =
-                (kEpi == EPI_SILU_MUL ? silu_f(r[2 * i + 1]) : gelu_tanh_f(r[2 * i + 1])) * r[32 + 2 * i + 1];
+                (kE == EPI_SILU_MUL ? silu_f(r[2 * i + 1]) : gelu_tanh_f(r[2 * i + 1])) * r[32 + 2 * i + 1];
             out16[i] = ptx::pack_bf16x2(a0, a1);
           }
         } else {
-          if constexpr (kEpi == EPI_RS) {
+          if constexpr (kE == EPI_RS) {
             if (add_mask) {
               const int col = out_col0 + pc * 32;
               for (int s2 = 0; s2 < p.world; ++s2)       // own fp32 partial + slots, ascending rank
                 if (add_mask & (1u << s2)) add_slot32(r, stg + ((size_t)s2 * p.M_r + myrow) * p.N_out, col, p.N_out);
             }
           }
-          if constexpr (kEpi == EPI_MOE_SCATTER) {
+          if constexpr (kE == EPI_MOE_SCATTER) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) r[i] *= moe_wt;   // top-k weight, applied before the bf16 transport
           }
@@ -668,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         if (pc + 2 == pc_end) release_tmem();
         else epi_load<kGated>(tacc, pc + 2, ra_);
         compute(rb_, pc + 1, pk + 16);
-        if constexpr (kEpi == EPI_MOE_SCATTER) {
+        if constexpr (kE == EPI_MOE_SCATTER) {
           // tile_push_data p2p of weighted row segments to the owners' staging slots.  The warp's 32
           // rows x 64 columns are transposed through its smem buffer so that every store instruction
           // writes 4 whole 128-byte row segments (coalesced) instead of 32 scattered 16-byte pieces.
@@ -700,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         }
         if (pc + 2 < pc_end) ptx::tmem_ld_wait_fence<kPW>(ra_);
       }
-      if constexpr (kEpi == EPI_RS) {
+      if constexpr (kE == EPI_RS) {
         // peer_tile_notify per warp slice: once every byte this warp pushed has landed in the
         // target's slot (its own bulk groups complete), release its slice flag(s).  The TMEM
         // buffer was already released, so the wait overlaps the next tile's MMAs.
@@ -727,6 +781,31 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
         __syncwarp();
       }
       if (cta_in_pair == 0 && ew == 0 && lane == 0) trace_ev(p.trace, TU_COMPUTE, TK_TILE_END, rank, item);
+      };   // body
+      if constexpr (kFused) {
+        if (!ph2) {
+          body(std::integral_constant<int, kEpi>{});
+          // this warp's Z rows of the tile have landed (stores complete, not just read): count them into
+          // the m-block's counter (release, gpu scope) for the phase-2 producers' acquire
+          // (counted in output columns stored, so a sub-tile past N adds 0: every warp's total per m-block
+          // and call is N_out whatever the tile split)
+          if (lane == 0) {
+            constexpr int sw = (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) ? 128 : 256;
+            const int c0 = (nb * kNSub + sub_lo) * sw;
+            const int cols = max(0, min(p.N_out, c0 + sub_n * sw) - c0);
+            ptx::bulk_wait<0>();
+            ptx::fence_proxy_async_global();
+            ptx::red_release_gpu_add(p.zdone[lr] + mb, (unsigned)cols);
+          }
+          __syncwarp();
+        } else if (epi == EPI_RS) {
+          body(std::integral_constant<int, EPI_RS>{});
+        } else {
+          body(std::integral_constant<int, EPI_STORE>{});
+        }
+      } else {
+        body(std::integral_constant<int, kEpi>{});
+      }
     }
     if (lane == 0) ptx::bulk_wait<0>();
     __syncwarp();
@@ -763,6 +842,18 @@ __global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_const
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kPair>(tmem_base, 512);
   }
+}
+
+template <int kPair, int kStages, int kEpi, bool kAG, int kNSub, int kMoE = MOE_NONE>
+__global__ void __launch_bounds__(kThreads, 1) tl_gemm_kernel(const __grid_constant__ Params p) {
+  gemm_body<kPair, kStages, kEpi, kAG, kNSub, kMoE, false>(p, p);
+}
+
+// The fused MLP layer (tl_mlp_forward): phase 1 = AG + GEMM1 + activation (p1), phase 2 = GEMM2 + RS (p2).
+template <int kPair, int kStages, int kEpi, bool kAG, int kNSub>
+__global__ void __launch_bounds__(kThreads, 1) tl_mlp_kernel(const __grid_constant__ Params p1,
+                                                            const __grid_constant__ Params p2) {
+  gemm_body<kPair, kStages, kEpi, kAG, kNSub, MOE_NONE, true>(p1, p2);
 }
 
 // Dynamic tile-centric mapping for the MoE first half ("lookup tables, whose values can

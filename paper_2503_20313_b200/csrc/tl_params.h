@@ -17,7 +17,10 @@ enum Epi : int { EPI_STORE = 0, EPI_SILU_MUL = 1, EPI_GELU_MUL = 2, EPI_RS = 3, 
 // MoE kernel flavours: 1 = AG + gather + GroupGEMM (rows gathered by token id), 2 = grouped GEMM
 // whose epilogue scatters weighted rows to the owners' staging slots (GroupGEMM + Scatter + TopK + RS)
 enum MoeKind : int { MOE_NONE = 0, MOE_GATHER = 1, MOE_SCATTER = 2 };
-enum Order : int { ORDER_IDENTITY = 0, ORDER_AG_INTERLEAVE = 1, ORDER_ROTATE = 2 };
+// ORDER_RS_INTERLEAVE (phase 2 of the fused MLP kernel): block `loc` of every remote owner in ring order
+// (r+1, r+2, ...), loc by loc -- the order in which phase 1 (ORDER_AG_INTERLEAVE) finishes their Z rows --
+// and the own owner block last (every remote partial leaves before an own tile waits).
+enum Order : int { ORDER_IDENTITY = 0, ORDER_AG_INTERLEAVE = 1, ORDER_ROTATE = 2, ORDER_RS_INTERLEAVE = 3 };
 // RS_DMA: the hybrid binding the paper benchmarks for GEMM+RS ("scatter is done using DMA, and
 // reduction is done on SMs"): remote partial tiles go to a local outbox, a per-(owner, 128-row block)
 // counter releases a flag, the copy engines move each finished block to the owner (host-enqueued
@@ -84,6 +87,11 @@ struct alignas(64) Params {
   int topk;           // MoE: routed slots per token
   unsigned int moe_done_base;       // MoE scatter: counter value before this call
   uint32_t* moe_flags[kMaxWorld];   // MoE scatter: [W slots] completion flags of rank o
+  // fused MLP kernel (tl_mlp_kernel): per local rank, one counter per 256-row m-block of Z, raised by
+  // the phase-1 epilogue warps (sub-tiles stored) and awaited by the phase-2 producers (monotone across
+  // calls: the target is calls x per-call count)
+  uint32_t* zdone[kMaxWorld];
+  uint32_t zdone_target;
 };
 
 }  // namespace tl

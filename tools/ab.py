@@ -33,8 +33,7 @@ def main():
     Z = torch.empty(M, il, device="cuda", dtype=torch.bfloat16)
     out = torch.empty(M, H, device="cuda", dtype=torch.bfloat16)
     f1, f2 = 2 * M * H * 2 * il, 2 * M * il * H
-    flops = {"g1": f1, "g2": f2, "layer": f1 + f2, "cublas_g1": f1, "cublas_g2": f2}[op if op in ("g1", "g2", "layer")
-                                                                                      else op]
+    flops = {"g1": f1, "g2": f2, "layer": f1 + f2, "mlp": f1 + f2}[op]
     comms = []
     for cfg in cfgs:
         c = tl.Comm.single(0, max_M=M, max_H=H)
@@ -47,10 +46,13 @@ def main():
     def run(ci):
         c = comms[ci]
         if cfgs[ci] == "cublas":
-            if op in ("g1", "layer"):
+            if op in ("g1", "layer", "mlp"):
                 torch.matmul(x, w1.T, out=y)
-            if op in ("g2", "layer"):
+            if op in ("g2", "layer", "mlp"):
                 torch.matmul(Z, w2.T, out=out)
+            return
+        if op == "mlp":      # tl_mlp_forward (one fused launch unless mlp_fused = 0)
+            c.mlp_forward(x, w1, w2, out, act=tl.ACT_SILU_MUL, Z=Z)
             return
         if op in ("g1", "layer"):
             c.ag_gemm(x, w1, Z, act=tl.ACT_SILU_MUL)
