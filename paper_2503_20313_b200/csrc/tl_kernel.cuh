@@ -478,7 +478,10 @@ __device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
         const int as = it % kAccBufs;
         ptx::mbar_wait(&tempty[as], ((it / kAccBufs) & 1) ^ 1);
         ptx::tc_fence_after();
-        if (lane == 0) trace_ev(p.trace, TU_COMPUTE, TK_TILE_START, rank, item);
+        if (lane == 0) {
+          trace_ev(p.trace, TU_COMPUTE, TK_TILE_START, rank, item);
+          trace_clock(p.trace, rank, item);
+        }
         const uint32_t tmem_d = tmem_base + as * kAccCols;
         auto issue = [&](auto ns_c, int s_lo) {
           constexpr int NS = decltype(ns_c)::value;

@@ -107,7 +107,7 @@ struct TraceEv {
 };
 enum TraceUnit : int { TU_COMPUTE = 0, TU_COPY = 1 };
 enum TraceKind : int { TK_TILE_START = 0, TK_TILE_END = 1, TK_WAIT_START = 2, TK_WAIT_END = 3, TK_NOTIFY = 4,
-                       TK_COPY_START = 5, TK_COPY_END = 6 };
+                       TK_COPY_START = 5, TK_COPY_END = 6, TK_SM_CLOCK = 7 };
 __device__ __forceinline__ void trace_ev(TraceBuf* tb, int unit, int kind, int rank, int tile, int peer = 0) {
   if (tb == nullptr) return;
   const unsigned long long i = atomicAdd(&tb->cursor, 1ull);
@@ -118,6 +118,21 @@ __device__ __forceinline__ void trace_ev(TraceBuf* tb, int unit, int kind, int r
     ev->rank = (unsigned short)rank;
     ev->unit = (unsigned char)unit;
     ev->kind = (unsigned char)kind;
+  }
+}
+
+// The SM's clock64 at a tile start (kind TK_SM_CLOCK, t_ns = cycles), next to the TK_TILE_START record:
+// tile periods in cycles separate "slower clock" from "fewer MMAs per cycle" (tools/tile_timeline.py).
+__device__ __forceinline__ void trace_clock(TraceBuf* tb, int rank, int tile) {
+  if (tb == nullptr) return;
+  const unsigned long long i = atomicAdd(&tb->cursor, 1ull);
+  if (i < tb->cap) {
+    TraceEv* ev = reinterpret_cast<TraceEv*>(tb + 1) + i;
+    ev->t_ns = clock64();
+    ev->tile = (unsigned)(tile & 0xFFFFFF);
+    ev->rank = (unsigned short)rank;
+    ev->unit = (unsigned char)TU_COMPUTE;
+    ev->kind = (unsigned char)TK_SM_CLOCK;
   }
 }
 

@@ -13,11 +13,11 @@ import numpy as np
 from ._lib import check, lib
 
 UNITS = ("compute", "copy")
-KINDS = ("tile_start", "tile_end", "wait_start", "wait_end", "notify", "copy_start", "copy_end")
+KINDS = ("tile_start", "tile_end", "wait_start", "wait_end", "notify", "copy_start", "copy_end", "sm_clock")
 _REC = np.dtype([("t_ns", "<u8"), ("tile", "<u4"), ("rank", "<u2"), ("unit", "u1"), ("kind", "u1")])
 
 
-def read_events(comm, cap: int | None = None):
+def read_events(comm, cap: int | None = None, clocks: bool = False):
     """Drain the comm's device trace into a list of SPEC TraceEvent dicts
     {"rank", "unit", "kind", "tile", "channel", "t_ns"} (+ "peer" for copy / notify events),
     sorted by time.  `channel` is left None: it follows from the tile through the static mapping."""
@@ -28,6 +28,8 @@ def read_events(comm, cap: int | None = None):
     out = []
     for r in buf[:n.value]:
         kind = KINDS[int(r["kind"])]
+        if kind == "sm_clock" and not clocks:   # SM cycle stamps (t_ns holds clock64), diagnostics only
+            continue
         ev = {"rank": int(r["rank"]), "unit": UNITS[int(r["unit"])], "kind": kind,
               "tile": int(r["tile"]) & 0xFFFFFF, "channel": None, "t_ns": int(r["t_ns"])}
         if kind in ("copy_start", "copy_end", "notify"):

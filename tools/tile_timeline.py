@@ -50,7 +50,9 @@ def main():
     c.set_option("trace_events", 1 << 15)   # realloc -> empty
     run()
     torch.cuda.synchronize()
-    ev = read_events(c)
+    ev = read_events(c, clocks=True)
+    clk = {e["tile"]: e["t_ns"] for e in ev if e["kind"] == "sm_clock"}
+    ev = [e for e in ev if e["kind"] != "sm_clock"]
     st = [e for e in ev if e["kind"] == "tile_start"]
     en = [e for e in ev if e["kind"] == "tile_end"]
     t0 = min(e["t_ns"] for e in st)
@@ -72,7 +74,18 @@ def main():
     if dur:
         print(f"start-to-start per pair (us): min {min(dur)/1e3:.2f} med {statistics.median(dur)/1e3:.2f} "
               f"max {max(dur)/1e3:.2f}")
-    kb = c.get_option("n_sub")
+    # tile periods in SM cycles (clock64 at each MMA tile start) and the implied SM clock
+    tstart = {e["tile"]: e["t_ns"] for e in st}
+    cyc, mhz = [], []
+    for p in by_pair:
+        its = sorted(i for k, i, _ in by_pair[p] if k == "s")
+        for a_, b_ in zip(its, its[1:]):
+            if a_ in clk and b_ in clk:
+                cyc.append(clk[b_] - clk[a_])
+                mhz.append((clk[b_] - clk[a_]) / max(1, tstart[b_] - tstart[a_]) * 1e3)
+    if cyc:
+        print(f"tile period (SM cycles): min {min(cyc)} med {statistics.median(cyc)} max {max(cyc)}; "
+              f"implied SM clock med {statistics.median(mhz):.0f} MHz")
     for p in sorted(by_pair)[:2]:
         print(p, [(k, i, round(t / 1e3, 1)) for k, i, t in sorted(by_pair[p], key=lambda z: z[2])])
 
