@@ -485,24 +485,19 @@ __device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
         const uint32_t tmem_d = tmem_base + as * kAccCols;
         auto issue = [&](auto ns_c, int s_lo) {
           constexpr int NS = decltype(ns_c)::value;
+          // the whole warp runs the loop with uniform operands; one elected lane issues each k-block's
+          // MMAs and commits (ptx::mma_kblock_elect)
           for (int kb = 0; kb < p.k_blocks; ++kb) {
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
-            if (lane == 0) {
-              const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(smem + L::off_a + stage * kAStage));
-              const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(smem + L::off_b + stage * L::kBStage)) +
-                                  s_lo * (L::kBBox >> 4);
-              const uint32_t td = tmem_d + s_lo * kUmmaN;
-#pragma unroll
-              for (int k = 0; k < kBK / 16; ++k)
-#pragma unroll
-                for (int q = 0; q < NS; ++q)
-                  ptx::mma_bf16<kPair>(ad + 2 * k, bd + q * (L::kBBox >> 4) + 2 * k, td + q * kUmmaN, idesc,
-                                       (kb | k) != 0);
-              ptx::mma_commit<kPair>(&empty[stage]);
-              if (kb == p.k_blocks - 1) ptx::mma_commit<kPair>(&tfull[as]);
-            }
-            __syncwarp();
+            const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(smem + L::off_a + stage * kAStage));
+            const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(smem + L::off_b + stage * L::kBStage)) +
+                                s_lo * (L::kBBox >> 4);
+            const uint32_t td = tmem_d + s_lo * kUmmaN;
+            static_assert(kBK == 64, "four K16 steps per k-block");
+            ptx::mma_kblock_elect<kPair, NS, (L::kBBox >> 4)>(ad, bd, td, idesc, kb != 0);
+            ptx::mma_commit_elect<kPair>(&empty[stage]);
+            if (kb == p.k_blocks - 1) ptx::mma_commit_elect<kPair>(&tfull[as]);
             if (++stage == kStages) stage = 0, phase ^= 1;
           }
         };

@@ -278,6 +278,72 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
   }
 }
+// One k-block (64 of K = 4 x K16 steps) of MMAs for NS 256-column sub-tiles in ONE asm block, issued by
+// one elected lane of a warp that runs the loop with warp-uniform operands: the descriptors advance inside
+// PTX (+32 B per K16 step = +2 in descriptor units; sub-tile q's B at +kBStride units, its accumulator at
+// +256 TMEM columns), so there is no per-MMA elect / register-broadcast waterfall.  The first step of each
+// sub-tile accumulates iff `acc` (k-block > 0).  Measured: the per-MMA `if (lane == 0)` issue cost ~100
+// cycles per k-block (82 % of the MMA rate on 256-wide tiles, tools/tile_timeline.py).
+template <int kPair, int NS, int kBStride>
+__device__ __forceinline__ void mma_kblock_elect(uint64_t ad, uint64_t bd, uint32_t td, uint32_t idesc, uint32_t acc) {
+#define TL_MMA_K1(OP)                                                                                     \
+  asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"                           \
+               "setp.ne.b32 p, %4, 0;\n\t"                                                                 \
+               "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"                        \
+               "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"                        \
+               "elect.sync _|e, 0xffffffff;\n\t"                                                           \
+               "@e " OP " [%0], %1, %2, %3, p;\n\t"                                                        \
+               "@e " OP " [%0], a1, b1, %3, 1;\n\t"                                                        \
+               "@e " OP " [%0], a2, b2, %3, 1;\n\t"                                                        \
+               "@e " OP " [%0], a3, b3, %3, 1;\n\t}" ::"r"(td),                                            \
+               "l"(ad), "l"(bd), "r"(idesc), "r"(acc)                                                      \
+               : "memory")
+#define TL_MMA_K2(OP)                                                                                     \
+  asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3, c0, c1, c2, c3;\n\t.reg .b32 u;\n\t" \
+               "setp.ne.b32 p, %4, 0;\n\t"                                                                 \
+               "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"                        \
+               "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"                        \
+               "add.s64 c0, %2, %5;\n\tadd.s64 c1, c0, 2;\n\tadd.s64 c2, c0, 4;\n\tadd.s64 c3, c0, 6;\n\t" \
+               "add.s32 u, %0, 256;\n\t"                                                                   \
+               "elect.sync _|e, 0xffffffff;\n\t"                                                           \
+               "@e " OP " [%0], %1, %2, %3, p;\n\t"                                                        \
+               "@e " OP " [u], %1, c0, %3, p;\n\t"                                                         \
+               "@e " OP " [%0], a1, b1, %3, 1;\n\t"                                                        \
+               "@e " OP " [u], a1, c1, %3, 1;\n\t"                                                         \
+               "@e " OP " [%0], a2, b2, %3, 1;\n\t"                                                        \
+               "@e " OP " [u], a2, c2, %3, 1;\n\t"                                                         \
+               "@e " OP " [%0], a3, b3, %3, 1;\n\t"                                                        \
+               "@e " OP " [u], a3, c3, %3, 1;\n\t}" ::"r"(td),                                             \
+               "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "n"(kBStride)                                      \
+               : "memory")
+  if constexpr (NS == 1) {
+    if constexpr (kPair == 2) TL_MMA_K1("tcgen05.mma.cta_group::2.kind::f16");
+    else TL_MMA_K1("tcgen05.mma.cta_group::1.kind::f16");
+  } else {
+    static_assert(NS == 2, "one or two sub-tiles");
+    if constexpr (kPair == 2) TL_MMA_K2("tcgen05.mma.cta_group::2.kind::f16");
+    else TL_MMA_K2("tcgen05.mma.cta_group::1.kind::f16");
+  }
+#undef TL_MMA_K1
+#undef TL_MMA_K2
+}
+// tcgen05.commit from one elected lane of a converged warp (pair mode: multicast to both CTAs' barriers).
+template <int kPair>
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+  if constexpr (kPair == 2) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+  }
+}
 // 32 lanes x 32 consecutive fp32 columns: thread i of the warp gets TMEM lane (base + i).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
