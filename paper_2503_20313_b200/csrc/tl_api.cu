@@ -410,9 +410,11 @@ void set_items(Params& p, int nsub, int n_pairs) {
 
 // Number of 256-column MMA sub-tiles per tile (option n_sub, 0 = auto), from a time model fitted
 // to B200 A/B runs (profiles/r01_perf_sweep*.log), in units of one 256-wide k-block of MMAs:
-// 256-wide tiles (TMEM double-buffered, epilogue hidden) cost 1.12 per k-block (extra L2->SMEM
-// traffic); 512-wide tiles cost 2 per k-block plus ~9 for the un-overlapped epilogue; half items
-// (split tail) cost 1 per k-block plus ~4.5.
+// 256-wide tiles (TMEM double-buffered, epilogue hidden) cost 1.04 per k-block (the MMA issue now runs
+// at 98 % of the MMA bound, tools/tile_timeline.py; the rest is the third more L2->SMEM bytes per FLOP,
+// i.e. power under the 1 kW cap -- refit on profiles/r02_ab_nsub_after_mma_issue.jsonl, was 1.12 with the
+// round-1 per-MMA issue); 512-wide tiles cost 2 per k-block plus ~9 for the un-overlapped epilogue; half
+// items (split tail) cost 1 per k-block plus ~4.5.
 // Model time (in 256-wide k-block units) of the GEMM with 256-wide (nsub 1) and 512-wide (nsub 2) tiles.
 void nsub_costs(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gated, bool rs, double& t1, double& t2);
 
@@ -431,7 +433,7 @@ void nsub_costs(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gate
   const int64_t bn1 = gated ? 128 : 256;
   const int64_t T1 = m_blocks * ((N_out + bn1 - 1) / bn1);
   const int64_t T2 = m_blocks * ((N_out + 2 * bn1 - 1) / (2 * bn1));
-  t1 = (double)((T1 + P - 1) / P) * 1.12 * kb;
+  t1 = (double)((T1 + P - 1) / P) * 1.04 * kb;
   const int64_t rem = T2 % P;
   // un-overlapped epilogue of a 512-wide tile: ~9 k-blocks for the gated (activation) and the
   // reduce-scatter epilogues, ~3.5 for a plain store (refit on the TP-2..8 rank shapes:
