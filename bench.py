@@ -357,8 +357,6 @@ def run_layer(args, ctx, M, emit=True):
     if x.numel() * 2 + w1.numel() * 2 + w2.numel() * 2 <= 126e6:   # small shapes: flush L2 between steps
         flush = torch.empty(128 * 2 ** 20, device="cuda", dtype=torch.int16)
 
-    fused = bool(comm.get_option("mlp_fused"))
-
     def step():   # tl_mlp_forward: one fused launch (AG + GEMM1 + SiLU*up, then GEMM2 + RS)
         comm.mlp_forward(x, w1, w2, out, act=act, Z=Z, stream=stream)
 
@@ -374,6 +372,8 @@ def run_layer(args, ctx, M, emit=True):
     for _ in range(args.warmup):
         step()
     barrier()
+    fused = comm.get_option("mlp_launches") == 1     # auto mode picked the fused launch for this shape
+    mlp_fused_opt = comm.get_option("mlp_fused")
 
     # ---- timed region: K steps, CUDA events around each layer launch on the launching stream
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
@@ -421,7 +421,7 @@ def run_layer(args, ctx, M, emit=True):
         comm.gemm_rs(Z, w2, out, stream=stream)
         bk[i][2].record(stream)
     barrier()
-    comm.set_option("mlp_fused", int(fused))
+    comm.set_option("mlp_fused", mlp_fused_opt)
     k1_ms = max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in bk) / args.steps)
     k2_ms = max_over_ranks(sum(e[1].elapsed_time(e[2]) for e in bk) / args.steps)
     comm.mlp_forward(x, w1, w2, out, act=act, Z=Z, stream=stream)   # `out` from the product path again
@@ -559,7 +559,8 @@ def run_layer(args, ctx, M, emit=True):
         cpu = cpu_baseline_leg(hX, hW1, hW2, act, fpr, M, args.cpu_seconds)
     barrier()
     opts = {k: comm.get_option(k) for k in ("cta_pair", "n_sub", "raster_group", "comm_tile_rows", "ag_binding",
-                                            "rs_binding", "rs_order")}
+                                            "rs_binding", "rs_order", "ag_mode", "mlp_fused")}
+    opts["mlp_launches"] = 1 if fused else 2
     comm.close()
     if rank != 0:
         return None

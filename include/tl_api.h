@@ -118,6 +118,11 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *   "debug_drop_rank"  see above
  *   "ag_binding"       AllGather resource binding: 0 = SMs (bulk-copy warp in every CTA),
  *                      1 = copy engines (cudaMemcpyAsync + stream write-value flags)
+ *   "mlp_fused"        tl_mlp_forward as ONE persistent launch (AG + GEMM1 + act tiles, then GEMM2 + RS tiles
+ *                      that wait on per-row-block counters of the first phase): 0 = two launches, 1 = auto
+ *                      (fused while the layer is <= 40 waves of tiles; default), 2 = always.  Bitwise-identical
+ *                      results.  SM bindings, SiLU / none activations and cta_pair 2 only (else two launches).
+ *   "mlp_launches"     (read it, do not set it) kernels the last tl_mlp_forward launched: 1 fused, 2 separate
  *   "ag_mode"          AllGather data-transfer mode: 0 = push (tile_push_data: each
  *                      source's copy role writes its producer tiles into every rank's gathered buffer),
  *                      1 = pull (tile_pull_data: each rank's copy role reads every source's tiles from

@@ -154,7 +154,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 0, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, ag_mode = 0, mlp_fused = 1, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0;
+          n_sub = 0, ag_binding = 0, ag_mode = 0, mlp_fused = 1, mlp_launches = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0;
 };
 
 struct OptDesc {
@@ -176,7 +176,8 @@ const OptDesc kOpts[] = {
     {"n_sub", &Options::n_sub, 0, 2},
     {"ag_binding", &Options::ag_binding, 0, 1},
     {"ag_mode", &Options::ag_mode, 0, 1},
-    {"mlp_fused", &Options::mlp_fused, 0, 1},
+    {"mlp_fused", &Options::mlp_fused, 0, 2},
+    {"mlp_launches", &Options::mlp_launches, 0, 2},   // informational: kernels the last tl_mlp_forward used
     {"dma_tile_rows", &Options::dma_tile_rows, 0, 1 << 20},
     {"debug_mode", &Options::debug_mode, 0, 3},
     {"attn_poly", &Options::attn_poly, 0, 8},
@@ -958,6 +959,7 @@ tl_status mlp_impl(tl_comm* c, const void* const* X, const void* const* W1, cons
   // two kernels.
   const bool fused = c->opt.mlp_fused && pair_of(c) == 2 && act != TL_ACT_GELU_TANH_MUL && c->opt.ag_binding == 0 &&
                      c->opt.rs_binding == 0 && c->opt.debug_mode == 0 && M > 0 && H > 0 && I_l > 0;
+  c->opt.mlp_launches = 2;
   if (!fused) {
     st = ag_gemm_impl(c, X, W1, z, nullptr, M, I_l, H, act, stream);
     if (st != TL_OK) return st;
@@ -970,6 +972,24 @@ tl_status mlp_impl(tl_comm* c, const void* const* X, const void* const* W1, cons
     nsub_costs(c, M, I_l, H, act != TL_ACT_NONE, false, a1, a2);
     nsub_costs(c, M, H, I_l, false, c->world > 1, b1, b2);
     nsub = (a2 + b2 < a1 + b1) ? 2 : 1;
+  }
+  // auto (mlp_fused = 1): the fused launch saves a fill, a drain and GEMM1's partial last wave -- worth it
+  // while the layer is a few tens of waves (TP rank shapes: 7B TP-8 0.242 -> 0.208 ms); the long layers
+  // (70B at W = 1, ~55 waves) measured ~1.5 % faster as two launches, so they keep them.  (Decided before
+  // any epoch is consumed: the two paths must advance the AG / RS epochs identically.)
+  if (c->opt.mlp_fused == 1) {
+    const int64_t n_pairs = ctas_per_rank(c) / 2, mb = (M + 255) / 256;
+    auto items = [&](int64_t n_blocks) {
+      const int64_t T = mb * n_blocks, rem = T % n_pairs;
+      return (nsub == 2 && rem != 0 && 2 * rem <= n_pairs) ? T + rem : T;
+    };
+    const int64_t n1 = items((I_l + (act != TL_ACT_NONE ? 128 : 256) * nsub - 1) / ((act != TL_ACT_NONE ? 128 : 256) * nsub));
+    const int64_t n2 = items((H + 256 * nsub - 1) / (256 * nsub));
+    if (n1 + n2 > 40 * n_pairs) {
+      st = ag_gemm_impl(c, X, W1, z, nullptr, M, I_l, H, act, stream);
+      if (st != TL_OK) return st;
+      return gemm_rs_impl(c, z, W2, out, M, H, I_l, stream);
+    }
   }
   // validate both halves before either consumes an epoch
   if (H % 8) return fail(TL_ERR_INVALID, "H must be a multiple of 8");
@@ -1015,6 +1035,7 @@ tl_status mlp_impl(tl_comm* c, const void* const* X, const void* const* W1, cons
     for (int i = 0; i < c->n_local; ++i) pp[0].zdone[i] = pp[1].zdone[i] = c->zdone[i];
     pp[1].zdone_target = c->zdone_calls * (uint32_t)(8 * I_l);
     st = launch_mlp(c, pp[0], pp[1], act, c->world > 1, nsub, stream);
+    c->opt.mlp_launches = 1;
   }
   delete[] pp;
   return st;

@@ -54,7 +54,7 @@ def test_fused_equals_two_kernels(tl, W, act, nsub):
     c.set_option("n_sub", nsub)
     c.set_option("mlp_fused", 0)
     ref = _run(tl, c, xs, w1, w2, M, H, W, act)
-    c.set_option("mlp_fused", 1)
+    c.set_option("mlp_fused", 2)
     got = _run(tl, c, xs, w1, w2, M, H, W, act)
     for r in range(W):
         assert torch.equal(got[r], ref[r]), f"rank {r}"
@@ -75,7 +75,7 @@ def test_fused_ragged_shapes(tl, W, M):
     c.set_option("n_sub", 2)     # the same tile width on both paths (auto may pick per GEMM)
     c.set_option("mlp_fused", 0)
     ref = _run(tl, c, xs, w1, w2, M, H, W, act)
-    c.set_option("mlp_fused", 1)
+    c.set_option("mlp_fused", 2)
     got = _run(tl, c, xs, w1, w2, M, H, W, act)
     for r in range(W):
         assert torch.equal(got[r], ref[r]), f"rank {r}"
@@ -94,7 +94,7 @@ def test_fused_ring_and_pull(tl, W):
             c.set_option(k, v)
         c.set_option("mlp_fused", 0)
         ref = _run(tl, c, xs, w1, w2, M, H, W, act)
-        c.set_option("mlp_fused", 1)
+        c.set_option("mlp_fused", 2)
         got = _run(tl, c, xs, w1, w2, M, H, W, act)
         for r in range(W):
             assert torch.equal(got[r], ref[r]), f"{opts} rank {r}"
@@ -117,7 +117,7 @@ def test_fused_many_calls_and_shape_changes(tl):
         data[(M, I)] = [[t.cuda() for t in L] for L in (Xs, W1s, W2s)]
         c.set_option("mlp_fused", 0)
         refs[(M, I)] = _run(tl, c, *data[(M, I)], M, H, W, act)
-    c.set_option("mlp_fused", 1)
+    c.set_option("mlp_fused", 2)
     for rep in range(6):
         for M, I in cases:
             got = _run(tl, c, *data[(M, I)], M, H, W, act)
@@ -142,7 +142,7 @@ def test_fused_bitwise_under_perturbed_schedules(tl, W):
     c.set_option("n_sub", 2)
     c.set_option("mlp_fused", 0)
     ref = _run(tl, c, xs, w1, w2, M, H, W, act)
-    c.set_option("mlp_fused", 1)
+    c.set_option("mlp_fused", 2)
     for d in (1000, 20000):
         c.set_option("debug_delay_ns", d)
         for _ in range(3):
@@ -161,7 +161,7 @@ def test_fused_full_size_70b_w1(tl):
     c = tl.Comm.single(0, max_M=M, max_H=H)
     c.set_option("n_sub", 2)
     outs = []
-    for fused in (0, 1):
+    for fused in (0, 2):
         c.set_option("mlp_fused", fused)
         o = torch.empty(M, H, device="cuda", dtype=torch.bfloat16)
         c.mlp_forward(x, w1, w2, o, act=tl.ACT_SILU_MUL)
