@@ -332,12 +332,14 @@ __device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
         uint8_t* sa = smem + L::off_a + stage * kAStage;
         uint8_t* sb = smem + L::off_b + stage * L::kBStage;
         const int kc = kb * kBK;
+        // the whole warp runs this loop with uniform row ids (every lane loaded the same ones); one elected
+        // lane issues each gather (no per-instruction register-broadcast waterfall)
 #pragma unroll
         for (int i = 0; i < kGPer; ++i)
           if (i < ng)
-            ptx::tma_gather4<kPair>(&ra.tm_a, &full[stage], sa + (g0 + i) * 512, kc, ids4[i].x, ids4[i].y, ids4[i].z,
-                                    ids4[i].w);
-        if (is_main) {
+            ptx::tma_gather4_elect<kPair>(&ra.tm_a, &full[stage], sa + (g0 + i) * 512, kc, ids4[i].x, ids4[i].y,
+                                          ids4[i].z, ids4[i].w);
+        if (is_main && lane == 0) {
 #pragma unroll
           for (int sub = 0; sub < kNSub; ++sub) {   // one gathered A stage feeds kNSub 256-wide sub-tiles
             uint8_t* sbs = sb + sub * L::kBBox;
@@ -359,13 +361,14 @@ __device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
           else
             ptx::mbar_arrive_cluster(&full[stage], 0);
         }
+        __syncwarp();
         if (++stage == kStages) stage = 0, phase ^= 1;
       }
     }
   };
 
   if (kMoE == MOE_GATHER && (warp == 0 || warp == 2 || (!kAG && warp == 3))) {
-    if (lane == 0) moe_produce(warp == 0, warp == 0 ? 0 : warp == 2 ? kGPer : 2 * kGPer);
+    moe_produce(warp == 0, warp == 0 ? 0 : warp == 2 ? kGPer : 2 * kGPer);   // whole warps (elected issue)
   } else if (warp == 0) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
