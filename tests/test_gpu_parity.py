@@ -607,3 +607,25 @@ def test_debug_options_not_read_from_env(tl, monkeypatch):
     assert c.get_option("debug_drop_notify") == -1
     assert c.get_option("comm_tile_rows") == 128
     c.close()
+
+
+def test_parity_check_rejects_a_corrupted_gpu_tile(tl):
+    """Negative control on real GPU output: the element-wise parity check of every GPU test accepts the
+    fused layer's output and rejects the same output with ONE 128 x 256 tile scaled by 1 % (which the
+    global relative-Frobenius norm alone accepts)."""
+    from parity import parity_report
+    W, M, H, I = 4, 2048, 1024, 2048
+    X, G, U, W2 = TI.mlp_full(M, H, I, seed=21)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL)
+    c = tl.Comm.loopback(W, 0, max_M=M, max_H=H)
+    outs = [empty(M // W, H) for _ in range(W)]
+    c.mlp_forward_lb([cuda(x) for x in Xs], [cuda(w) for w in W1s], [cuda(w) for w in W2s], outs, act=TI.ACT_SILU_MUL)
+    assert c.check()[0] == 0
+    ref = np.concatenate(O.mlp_forward([TI.to_f64(t) for t in Xs], [TI.to_f64(t) for t in W1s],
+                                       [TI.to_f64(t) for t in W2s], TI.ACT_SILU_MUL), 0)
+    got = torch.cat(outs).double().cpu().numpy()
+    assert parity_report(got, ref)["ok"]
+    bad = got.copy()
+    bad[640:768, 512:768] *= 1.01
+    rep = parity_report(bad, ref)
+    assert not rep["ok"] and rep["worst_tile"] == (640, 512) and rep["global"] < TOL
