@@ -350,6 +350,9 @@ def run_layer(args, ctx, M, emit=True):
     Z = torch.empty(M, Il, device="cuda", dtype=torch.bfloat16)
     if distributed:
         comm = tl.Comm.from_process_group(None, dev, M, H)
+        if ctx.get("shared"):
+            comm.set_option("num_ctas", max(2, 148 // W // 2 * 2))
+            comm.set_option("timeout_ms", 120000)
     else:
         comm = tl.Comm.single(dev, M, H)
     stream = torch.cuda.current_stream()
@@ -449,7 +452,10 @@ def run_layer(args, ctx, M, emit=True):
     # ---- parity of this run's output against the fp64 oracle: every rank's block is sampled (rows
     # spread over the block + one whole 128-row tile of rank 0), per element and per row
     parity = None
-    if distributed:
+    if distributed and ctx.get("shared"):   # gloo: gather through host memory
+        full = torch.empty(M, H, dtype=torch.bfloat16)
+        dist.all_gather_into_tensor(full, out.cpu())
+    elif distributed:
         full = torch.empty(M, H, device="cuda", dtype=torch.bfloat16)
         dist.all_gather_into_tensor(full, out)
     else:
@@ -567,7 +573,10 @@ def run_layer(args, ctx, M, emit=True):
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "TFLOPS", "n_gpus": W, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) activations, N(0,1/fan_in) weights, "
+        "vs_baseline": None, "dtype": "bf16",
+        **({"mode": "TL_BENCH_SHARED_GPU code-path check: all ranks time-share cuda:0, not a measurement"}
+           if ctx.get("shared") else {}),
+        "data": "synthetic (seeded N(0,1) activations, N(0,1/fan_in) weights, "
                                                   "bf16; random-init weights of the named shape)",
         "config": cfg,
         "options": opts,
@@ -725,7 +734,15 @@ def main(argv=None):
     import torch.distributed as dist
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     distributed = world_env > 1
-    if distributed:
+    # TL_BENCH_SHARED_GPU=1 (code-path check only, never a measurement): every rank on cuda:0 with a share
+    # of the SMs, gloo instead of NCCL (which refuses two ranks on one device), no NCCL baseline
+    shared = distributed and os.environ.get("TL_BENCH_SHARED_GPU") == "1"
+    if shared:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        rank, W = dist.get_rank(), dist.get_world_size()
+        args.no_baseline = True
+    elif distributed:
         local = int(os.environ.get("LOCAL_RANK", "0"))
         if local >= torch.cuda.device_count():
             raise RuntimeError(f"rank {local} needs cuda:{local}, only {torch.cuda.device_count()} device(s) visible")
@@ -735,7 +752,7 @@ def main(argv=None):
     else:
         torch.cuda.set_device(0)
         rank, W = 0, 1
-    ctx = {"rank": rank, "W": W, "distributed": distributed, "dev": torch.cuda.current_device()}
+    ctx = {"rank": rank, "W": W, "distributed": distributed, "dev": torch.cuda.current_device(), "shared": shared}
     Ms = MSWEEP if args.msweep else [args.M or CONFIGS[args.config]["M"]]
     for M in Ms:
         if args.msweep:

@@ -434,12 +434,17 @@ void nsub_costs(const tl_comm* c, int64_t M, int64_t N_out, int64_t K, bool gate
   const int64_t bn1 = gated ? 128 : 256;
   const int64_t T1 = m_blocks * ((N_out + bn1 - 1) / bn1);
   const int64_t T2 = m_blocks * ((N_out + 2 * bn1 - 1) / (2 * bn1));
-  t1 = (double)((T1 + P - 1) / P) * 1.04 * kb;
+  // 256-wide tiles: 1.02 per k-block measured in SM cycles (tile timeline, MMA issue from one elected
+  // lane), x 1.035 for the third more L2->SMEM bytes per FLOP they move -- energy, i.e. clock, under the
+  // 1 kW cap, which every sustained run hits (refit on profiles/r02_ab_nsub_*.jsonl: 512-wide wins on the
+  // long-K 70B shapes, 256-wide on the short-K / few-wave ones)
+  t1 = (double)((T1 + P - 1) / P) * 1.055 * kb;
   const int64_t rem = T2 % P;
-  // un-overlapped epilogue of a 512-wide tile: ~9 k-blocks for the gated (activation) and the
-  // reduce-scatter epilogues, ~3.5 for a plain store (refit on the TP-2..8 rank shapes:
-  // profiles/r01_nsub_ab.log, 512-wide 3-8 % faster where the old constant chose 256-wide)
-  const double epi = (gated || rs) ? 9.0 : 3.5;
+  // un-overlapped epilogue of a 512-wide tile: ~12 k-block units whatever the epilogue kind (tile
+  // periods of 137 k / 63.6 k SM cycles against 131 k / 57.3 k of MMAs: r02_tile_timeline_cycles_*)
+  (void)gated;
+  (void)rs;
+  const double epi = 12.0;
   const double full2 = 2.0 * kb + epi;
   t2 = (double)(T2 / P) * full2 + (rem == 0 ? 0.0 : (2 * rem <= P ? kb + epi / 2 : full2));
 }
