@@ -26,7 +26,7 @@ def check(c, name):
     assert st == 0, (name, diag)
 
 
-def mlp(W, binding):
+def mlp(W, binding, fused=1, pull=0):
     M, H, I = 512, 256, 768
     X, G, U, W2 = TI.mlp_full(M, H, I, seed=1)
     Xs, W1s, W2s = (cu(L) for L in TI.shard_mlp(X, G, U, W2, W, TI.ACT_SILU_MUL))
@@ -36,6 +36,8 @@ def mlp(W, binding):
         c.set_option("ag_binding", 1)
         c.set_option("rs_binding", 1)
         c.set_option("rs_dma_rows", 128)
+    c.set_option("mlp_fused", fused)     # 2: the one-launch layer kernel, 0: two launches
+    c.set_option("ag_mode", pull)        # 1: AllGather pull mode
     outs = [torch.empty(M // W, H, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
     c.mlp_forward_lb(Xs, W1s, W2s, outs, act=TI.ACT_SILU_MUL)
     check(c, "mlp")
@@ -43,7 +45,7 @@ def mlp(W, binding):
     h = torch.nn.functional.silu(Xf @ G.cuda().float().t()) * (Xf @ U.cuda().float().t())
     ref = h.bfloat16().float() @ W2.cuda().float().t()
     e = rel(torch.cat(outs, 0), ref)
-    print(f"mlp W={W} binding={binding}: rel {e:.2e}")
+    print(f"mlp W={W} binding={binding} fused={fused} pull={pull} launches={c.get_option('mlp_launches')}: rel {e:.2e}")
     assert e < 1e-2
     c.close()
 
@@ -101,12 +103,13 @@ def moe(W, binding):
     c.close()
 
 
-def attn(W, binding):
+def attn(W, binding, pull=0):
     S, heads = 256 * W, 2
     Qs, Ks, Vs = (cu(L) for L in TI.attention_inputs(S, heads, 128, W, seed=8))
     c = tl.Comm.loopback(W, 0, max_M=S, max_H=2 * heads * 128)
     c.set_option("timeout_ms", 600000)   # the sanitizer slows the spin-waits down
     c.set_option("ag_binding", binding)
+    c.set_option("ag_mode", pull)
     outs = [torch.empty_like(q) for q in Qs]
     tl.sp_attention_lb(c, Qs, Ks, Vs, outs)
     check(c, "attn")
@@ -123,10 +126,13 @@ def attn(W, binding):
 if __name__ == "__main__":
     worlds = [int(w) for w in sys.argv[1].split(",")] if len(sys.argv) > 1 else [2, 4]
     for W in worlds:
+        for fused, pull in ((2, 0), (0, 0), (2, 1), (0, 1)):
+            mlp(W, 0, fused, pull)
         for b in (0, 1):
             mlp(W, b)
             ag_rs(W, b)
             moe(W, b)
             attn(W, b)
+        attn(W, 0, pull=1)
     torch.cuda.synchronize()
     print("SANITIZE_OPS_DONE")
