@@ -473,6 +473,7 @@ def run_layer(args, ctx, M, emit=True):
         parity = check_rows(np.stack([got[i] for i in rows]), np.stack([ref[i] for i in rows]))
         parity["status"] = int(st)
     del full
+    barrier()   # rank 0's oracle work is done before any rank launches the next collective layer call
 
     # ---- end to end through the public API: every step copies its X shard in from pinned host memory
     # and its output back (paper_2503_20313_b200.pipeline.MLPPipeline: H2D of step i+1 and D2H of step
