@@ -151,7 +151,7 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *                      may overlap the previous kernel in the stream (they wait before any data access)
  *   "attn_poly"        tl_sp_attention: every n-th pair of exponentials is evaluated on the FMA pipe
  *                      (Cody-Waite + cubic) instead of MUFU (default 3; 0 = all on MUFU; 2,3,4,6,8).
- *                      Ragged shapes (S/world % 128 != 0) always use the default split (3); the
+ *                      Aligned and ragged (S/world % 128 != 0) shapes use the same split; the
  *                      option affects speed only, never results beyond rounding. */
 tl_status tl_set_option(tl_comm_t comm, const char* key, int64_t value);
 tl_status tl_get_option(tl_comm_t comm, const char* key, int64_t* value);

@@ -76,6 +76,17 @@ def test_attention_ragged(tl, W, S):
     assert _err(results[0], ref) < TOL
 
 
+@pytest.mark.parametrize("poly", [0, 2, 8])
+def test_attention_ragged_exp2_split(tl, poly):
+    """The ragged instantiation honours option attn_poly (every n-th exponential pair on the FMA pipe,
+    0 = all on MUFU): each split meets the bound, and the splits differ only by rounding."""
+    W, S, heads = 2, 2 * 200, 2
+    comm = _comm(tl, W, S, heads)
+    comm.set_option("attn_poly", poly)
+    results, ref = _run(tl, W, S, heads, comm=comm, seed=5)
+    assert _err(results[0], ref) < TOL
+
+
 def test_attention_ragged_no_store_beyond_rows(tl):
     """A partial last query tile writes only its S_r rows: the bytes after O are left untouched."""
     S, heads = 200, 2
