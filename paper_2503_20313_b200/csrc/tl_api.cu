@@ -154,7 +154,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 0, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, ag_mode = 0, mlp_fused = 1, mlp_launches = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0, attn_pair = 0;
+          n_sub = 0, ag_binding = 0, ag_mode = 0, mlp_fused = 1, mlp_launches = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0;
 };
 
 struct OptDesc {
@@ -181,7 +181,6 @@ const OptDesc kOpts[] = {
     {"dma_tile_rows", &Options::dma_tile_rows, 0, 1 << 20},
     {"debug_mode", &Options::debug_mode, 0, 3},
     {"attn_poly", &Options::attn_poly, 0, 8},
-    {"attn_pair", &Options::attn_pair, 0, 1},
     {"debug_delay_ns", &Options::debug_delay_ns, 0, 1000000},
     {"trace_events", &Options::trace_events, 0, 1ll << 28},
     {"pdl", &Options::pdl, 0, 1},
@@ -1580,10 +1579,6 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
   memset(&p, 0, sizeof(p));
   int cpr = c->opt.num_ctas > 0 ? (int)c->opt.num_ctas : c->sm_count / c->n_local;
   if (cpr * c->n_local > c->sm_count) cpr = c->sm_count / c->n_local;
-  // CTA-pair kernel (tl_attn2_kernel): 256-query tiles over a TPC pair; needs S/world % 256 == 0 and an
-  // even CTA count per rank (clusters of 2 never straddle ranks)
-  const bool pair2 = c->opt.attn_pair == 1 && S_r % 256 == 0 && cpr >= 2;
-  if (pair2) cpr &= ~1;
   p.ctas_per_rank = std::max(1, cpr);
   p.S = (int)S;
   p.S_r = (int)S_r;
@@ -1643,37 +1638,8 @@ tl_status attn_impl(tl_comm* c, const void* const* Q, const void* const* K, cons
     if ((st = make_tmap_nd(&ra.tm_q, Q[i], 3, dq, str, box_in)) != TL_OK) break;
     if ((st = make_tmap_nd(&ra.tm_k, kf, 3, dkv, str, box_in)) != TL_OK) break;
     if ((st = make_tmap_nd(&ra.tm_v, vf, 3, dkv, str, box_in)) != TL_OK) break;
-    const uint32_t box_k2[3] = {64, 1, 64};
-    if (pair2 && (st = make_tmap_nd(&ra.tm_k2, kf, 3, dkv, str, box_k2)) != TL_OK) break;
   }
-  if (st == TL_OK && pair2) {
-    const int pm = (int)c->opt.attn_poly;
-    auto pick = [&](auto k0, auto k2, auto k3, auto k4, auto k6, auto k8) {
-      return pm >= 8 ? k8 : pm >= 6 ? k6 : pm >= 4 ? k4 : pm == 3 ? k3 : pm >= 2 ? k2 : k0;
-    };
-    auto kern = comm ? pick(tl_attn2_kernel<true, 0>, tl_attn2_kernel<true, 2>, tl_attn2_kernel<true, 3>,
-                            tl_attn2_kernel<true, 4>, tl_attn2_kernel<true, 6>, tl_attn2_kernel<true, 8>)
-                     : pick(tl_attn2_kernel<false, 0>, tl_attn2_kernel<false, 2>, tl_attn2_kernel<false, 3>,
-                            tl_attn2_kernel<false, 4>, tl_attn2_kernel<false, 6>, tl_attn2_kernel<false, 8>);
-    const int smem = comm ? Attn2Layout<true>::smem_request : Attn2Layout<false>::smem_request;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(p.n_local * p.ctas_per_rank);
-      cfg.blockDim = dim3(kAttnThreads);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = 2;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      e = cudaLaunchKernelEx(&cfg, kern, p);
-    }
-    if (e != cudaSuccess) st = fail(TL_ERR_CUDA, "attention (CTA pair) launch: %s", cudaGetErrorString(e));
-  } else if (st == TL_OK) {
+  if (st == TL_OK) {
     // fraction of exponentials on the FMA pipe: every attn_poly-th pair (0 = all on MUFU)
     const int pm = (int)c->opt.attn_poly;
     auto pick = [&](auto k0, auto k2, auto k3, auto k4, auto k6, auto k8) {

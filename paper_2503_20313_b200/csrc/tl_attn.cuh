@@ -48,7 +48,6 @@ struct alignas(64) AttnRank {
   CUtensorMap tm_q;   // [S_r][heads][128] of this rank, 64 x 1 x 128 boxes
   CUtensorMap tm_k;   // [S][heads][128] gathered K (or the shard itself when world == 1)
   CUtensorMap tm_v;   // [S][heads][128] gathered V
-  CUtensorMap tm_k2;  // same tensor as tm_k, 64 x 1 x 64 boxes (CTA-pair kernel: 64 keys per CTA)
   uint8_t* o;         // [S_r][heads][128] output
   const uint8_t* k_shard;
   const uint8_t* v_shard;
@@ -646,419 +645,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1) tl_attn_kernel(const __grid_c
   if (warp == 10) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<1>(tmem, 512);
-  }
-}
-
-// ================================================================================================
-// CTA-pair kernel (tcgen05 cta_group::2), used when S/world % 256 == 0 (option attn_pair, default 1).
-//
-// Why a different schedule (measured, tools/scratch traces of the one-CTA kernel above): its KV-block
-// period is ~2900 cycles against the 2048-cycle MMA bound.  (1) With the softmax work removed the
-// period is still 2503: per block the two SS Q.K^T (2 x 64 KB), the P.V B operands (2 x 32 KB) and the
-// K/V TMA writes (64 KB) move 256 KB through shared memory = 128 B/clk, the SM's shared-memory
-// bandwidth.  (2) With it, each tile's chain softmax (~1550 cycles incl. TMEM load) -> last P.V half +
-// next S (768 MMA cycles) -> commit/wake latencies (~700) is longer than the other tile's MMA work, so
-// the tensor pipe idles: P_X(j) lives over S_X(j) in TMEM, and TMEM (512 columns) holds only S and O of
-// two tiles, so S_X(j+1) cannot be computed ahead.
-//
-// Here one 256-query tile runs on a cluster of two CTAs (one TPC): every product is ONE M = 256 MMA,
-// each CTA holding its 128 query rows, half of every K block (64 keys) and half of every V block (64 of
-// the 128 head-dim columns), so per SM and block shared memory moves 32 (Q) + 16 (K) + 16 (V) + 32 KB
-// (TMA) over 1024 MMA cycles (~78 B/clk).  With one tile, TMEM holds O (128 columns) and THREE S
-// buffers, so S(j+1), S(j+2) are computed while the softmax works on S(j): the softmax warps run block
-// after block without waiting, and S(j+3) only waits for P(j).V (in issue order).  Each of the 128
-// rows is shared by two softmax warps (warp w: TMEM lanes 32 (w%4).., key half w/4), which exchange
-// their half-row maxima through shared memory, so the per-block softmax latency halves.
-//   warps 0-7  softmax + epilogue (row group w%4, key / head-dim half w/4)
-//   warp 8     TMA producer of Q and K;  warp 11  TMA producer of V
-//   warp 9     MMA issuer (leader CTA only): S(j) = Q K_j^T (SS), O (+)= P(j) V_j (P from TMEM)
-//   warp 10    TMEM allocator + AG copy role (W > 1)
-// TMEM per CTA: O [0,128), S_b [128 + 128 b, 256 + 128 b), b = block % 3.  P(j) is packed bf16 over the
-// first half of each warp's own S columns (keys 0-63 -> columns 0-31, keys 64-127 -> 64-95).
-constexpr int kA2Stages = 4;
-constexpr int kA2Q = 0;                                // Q: this CTA's 128 rows (2 D halves of 16 KB)
-constexpr int kA2K = 32768;                            // K ring: 64 keys x 2 D halves (2 x 8 KB) per stage
-constexpr int kA2V = kA2K + kA2Stages * 16384;         // V ring: 128 keys x this CTA's 64 D columns
-constexpr int kA2Copy = kA2V + kA2Stages * 16384;      // AG copy staging (2 x 16 KB)
-template <bool kAG>
-struct Attn2Layout {
-  static constexpr int off_x = kA2Copy + (kAG ? 2 * 16384 : 0);   // row-max exchange [2][2][128] + l [2][128]
-  static constexpr int off_bar = off_x + 3 * 1024;
-  static constexpr int n_bars = 40;
-  static constexpr int off_tmem = off_bar + n_bars * 8;
-  static constexpr int smem_request = off_tmem + 16 + 1024;
-};
-
-// S = Q K^T for the pair's 256-query tile over a 128-key block (M = 256, N = 128, K = 128: 8 K16 steps).
-// A = Q (this CTA's 128 rows; D halves 16 KB apart), B = this CTA's 64 keys (D halves 8 KB apart).
-__device__ __forceinline__ void mma2_s8_elect(uint64_t adesc, uint64_t bdesc, uint32_t tmem_d, uint32_t idesc) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n\t"
-      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
-      "add.s64 a4, %1, 1024;\n\tadd.s64 a5, %1, 1026;\n\tadd.s64 a6, %1, 1028;\n\tadd.s64 a7, %1, 1030;\n\t"
-      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
-      "add.s64 b4, %2, 512;\n\tadd.s64 b5, %2, 514;\n\tadd.s64 b6, %2, 516;\n\tadd.s64 b7, %2, 518;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, 0;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a4, b4, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a5, b5, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a6, b6, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a7, b7, %3, 1;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc)
-      : "memory");
-}
-// Half of O (+)= P V for the pair: 4 K16 steps (64 keys); P from both CTAs' TMEM (+8 columns per
-// step), V from both CTAs' smem (each CTA's 64 head-dim columns, MN-major, +2 KB per step).
-__device__ __forceinline__ void mma2_pv4_elect(uint32_t tmem_a, uint64_t bdesc, uint32_t tmem_d, uint32_t idesc,
-                                               uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 t1, t2, t3;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "add.s64 b1, %2, 128;\n\tadd.s64 b2, %2, 256;\n\tadd.s64 b3, %2, 384;\n\t"
-      "add.s32 t1, %1, 8;\n\tadd.s32 t2, %1, 16;\n\tadd.s32 t3, %1, 24;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t1], b1, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t2], b2, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t3], b3, %3, 1;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-template <bool kAG, int kPolyMod>
-__global__ void __launch_bounds__(kAttnThreads, 1) tl_attn2_kernel(const __grid_constant__ AttnParams p) {
-  using L = Attn2Layout<kAG>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int lr = blockIdx.x / p.ctas_per_rank;
-  const int cta = blockIdx.x % p.ctas_per_rank;
-  const int cip = (int)ptx::cluster_ctarank();          // 0 = pair leader (issues the MMAs)
-  const int pair = cta / 2, n_pairs = p.ctas_per_rank / 2;
-  const AttnRank& ra = p.rk[lr];
-  const int rank = ra.rank;
-  const int nqt = p.S_r / 256, n_units = p.debug_mode == 2 ? 0 : p.heads * nqt;
-  const int n_kv = p.S / 128, bpr = p.S_r / 128;
-  const int bpc = 1;
-
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::off_bar);
-  uint64_t* q_full = bars + 0;     // leader: both CTAs' Q bytes
-  uint64_t* q_free = bars + 1;     // commit (multicast)
-  uint64_t* o_full = bars + 2;     // commit (multicast): the unit's last P.V done
-  uint64_t* o_free = bars + 3;     // leader: 16 softmax warps read O
-  uint64_t* k_full = bars + 4;     // [4] leader
-  uint64_t* k_empty = bars + 8;    // [4] commit (multicast)
-  uint64_t* v_full = bars + 12;    // [4] leader
-  uint64_t* v_empty = bars + 16;   // [4] commit (multicast)
-  uint64_t* s_full = bars + 20;    // [3] commit (multicast): S_b computed
-  uint64_t* o_step = bars + 23;    // [3] commit (multicast): P.V of the block in S_b done (lazy rescale)
-  // [3 buffers][2 key halves] leader: half h of P(g) written by its 8 warps (both CTAs).  Per buffer,
-  // because the softmax may run up to three blocks ahead of the P.V issue (S(g+3) waits for P(g).V):
-  // one barrier per half would complete several phases before the MMA warp waits on the first
-  uint64_t* p_ready = bars + 26;
-  uint64_t* cbar = bars + 32;      // [2] AG copy staging
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::off_tmem);
-  float* xmax = reinterpret_cast<float*>(smem + L::off_x);          // [2 parity][2 half][128 rows]
-  float* xsum = xmax + 512;                                           // [2 half][128 rows]
-
-  if (warp == 9 && lane == 0) {
-    ptx::mbar_init(q_full, 2);
-    ptx::mbar_init(q_free, 1);
-    ptx::mbar_init(o_full, 1);
-    ptx::mbar_init(o_free, 16);
-    for (int i = 0; i < kA2Stages; ++i) {
-      ptx::mbar_init(&k_full[i], 2);
-      ptx::mbar_init(&k_empty[i], 1);
-      ptx::mbar_init(&v_full[i], 2);
-      ptx::mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < 3; ++i) {
-      ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&o_step[i], 1);
-    }
-    for (int i = 0; i < 6; ++i) ptx::mbar_init(&p_ready[i], 8);
-    for (int i = 0; i < 2; ++i) ptx::mbar_init(&cbar[i], 1);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 8 && lane == 0) {
-    ptx::prefetch_tmap(&ra.tm_q);
-    ptx::prefetch_tmap(&ra.tm_k2);
-    ptx::prefetch_tmap(&ra.tm_v);
-  }
-  if (warp == 10) ptx::tmem_alloc<2>(tmem_slot, 512);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::cluster_sync();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  if (warp >= 8) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
-  }
-  if (warp == 8 || warp == 11) {
-    // ============================== TMA producers: Q + K (warp 8), V (warp 11) ==============================
-    if (lane == 0) {
-      const bool kq = warp == 8;
-      uint32_t g = 0, uses = 0;
-      for (int u = pair; u < n_units; u += n_pairs, ++uses) {
-        const int h = u / nqt, qt = u % nqt;
-        if (kq) {
-          ptx::mbar_wait(q_free, (uses & 1) ^ 1);
-          ptx::tma_load_3d<2>(&ra.tm_q, q_full, smem + kA2Q, 0, h, qt * 256 + cip * 128);
-          ptx::tma_load_3d<2>(&ra.tm_q, q_full, smem + kA2Q + 16384, 64, h, qt * 256 + cip * 128);
-          if (cip == 0) ptx::mbar_arrive_expect_tx(q_full, 2 * 32768);
-          else ptx::mbar_arrive_cluster(q_full, 0);
-        }
-        for (int j = 0; j < n_kv; ++j, ++g) {
-          const int kvb = attn_kv_block(j, rank, p.world, bpr, bpc);
-          if constexpr (kAG) {
-            if (kq) debug_delay(p.delay_ns, p.delay_seed, rank, 2 * j + 1);
-            if (p.debug_mode != 1) attn_wait_rows(p, rank, kvb * 128, kvb * 128 + 128);
-          }
-          const int st = g % kA2Stages;
-          const uint32_t ph = (g / kA2Stages) & 1;
-          if (kq) {
-            ptx::mbar_wait(&k_empty[st], ph ^ 1);
-            uint8_t* k = smem + kA2K + st * 16384;
-            ptx::tma_load_3d<2>(&ra.tm_k2, &k_full[st], k, 0, h, kvb * 128 + cip * 64);
-            ptx::tma_load_3d<2>(&ra.tm_k2, &k_full[st], k + 8192, 64, h, kvb * 128 + cip * 64);
-            if (cip == 0) ptx::mbar_arrive_expect_tx(&k_full[st], 2 * 16384);
-            else ptx::mbar_arrive_cluster(&k_full[st], 0);
-          } else {
-            ptx::mbar_wait(&v_empty[st], ph ^ 1);
-            uint8_t* v = smem + kA2V + st * 16384;
-            ptx::tma_load_3d<2>(&ra.tm_v, &v_full[st], v, cip * 64, h, kvb * 128);
-            if (cip == 0) ptx::mbar_arrive_expect_tx(&v_full[st], 2 * 16384);
-            else ptx::mbar_arrive_cluster(&v_full[st], 0);
-          }
-        }
-      }
-    }
-  } else if (warp == 9) {
-    // ============================== MMA issuer (leader CTA) ==============================
-    // Per unit: S(0), S(1), S(2) into S_0..2; then per block j: P(j).V in two key halves (each as soon
-    // as its 8 softmax warps have written it), then S(j+3) into the freed buffer.  Buffers and K/V
-    // stages are indexed by the CTA's global block counter g.
-    if (cip == 0) {
-      constexpr uint32_t idesc_s = ptx::idesc_bf16(256, 128);
-      constexpr uint32_t idesc_pv = ptx::idesc_bf16(256, 128) | (1u << 16);   // B (= V) MN-major
-      const uint64_t qd = ptx::smem_desc_sw128(ptx::smem_u32(smem + kA2Q));
-      uint32_t g = 0, uses = 0;
-      auto issue_s = [&](uint32_t gg) {   // S(gg) = Q K_gg^T into S_(gg % 3)
-        ptx::mbar_wait(&k_full[gg % kA2Stages], (gg / kA2Stages) & 1);
-        ptx::tc_fence_after();
-        mma2_s8_elect(qd, ptx::smem_desc_sw128(ptx::smem_u32(smem + kA2K + (gg % kA2Stages) * 16384)),
-                      tmem + 128 + (gg % 3) * 128, idesc_s);
-        ptx::mma_commit_elect<2>(&s_full[gg % 3]);
-        ptx::mma_commit_elect<2>(&k_empty[gg % kA2Stages]);
-      };
-      for (int u = pair; u < n_units; u += n_pairs, ++uses) {
-        ptx::mbar_wait(q_full, uses & 1);
-        for (int j = 0; j < 3 && j < n_kv; ++j) issue_s(g + j);
-        if (n_kv <= 3) ptx::mma_commit_elect<2>(q_free);
-        for (int j = 0; j < n_kv; ++j, ++g) {
-          const int st = g % kA2Stages;
-          const uint32_t tp = tmem + 128 + (g % 3) * 128;
-          const uint64_t vd = ptx::smem_desc_sw128_lbo(ptx::smem_u32(smem + kA2V + st * 16384), 16384, 1024);
-          ptx::mbar_wait(&v_full[st], (g / kA2Stages) & 1);
-          if (j == 0) ptx::mbar_wait(o_free, (uses & 1) ^ 1);
-          mbar_wait_fast(&p_ready[(g % 3) * 2], (g / 3) & 1);
-          ptx::tc_fence_after();
-          mma2_pv4_elect(tp, vd, tmem, idesc_pv, j == 0 ? 0u : 1u);
-          mbar_wait_fast(&p_ready[(g % 3) * 2 + 1], (g / 3) & 1);
-          ptx::tc_fence_after();
-          mma2_pv4_elect(tp + 64, vd + 512, tmem, idesc_pv, 1u);
-          ptx::mma_commit_elect<2>(&v_empty[st]);
-          ptx::mma_commit_elect<2>(&o_step[g % 3]);
-          if (j + 3 < n_kv) {
-            issue_s(g + 3);
-            if (j + 4 == n_kv) ptx::mma_commit_elect<2>(q_free);
-          }
-        }
-        ptx::mma_commit_elect<2>(o_full);
-      }
-    }
-  } else if (warp == 10) {
-    // ============================== AG copy role (K and V shards) ==============================
-    if constexpr (kAG) {
-      if (lane == 0 && cta < p.copy_ctas) {
-        uint8_t* cbuf = smem + kA2Copy;
-        uint32_t cph[2] = {0, 0};
-        int g = 0;
-        const int W = p.world;
-        const int n_tasks = p.tiles_per_rank * W;
-        for (int task = cta; task < n_tasks; task += p.copy_ctas) {
-          const int t = task / W, d = (rank + task % W) % W;
-          const bool pull = p.ag_mode == 1;
-          debug_delay(p.delay_ns, p.delay_seed, rank, 2 * task);
-          const int lo = t * p.tm_rows, hi = min(lo + p.tm_rows, p.S_r);
-          const uint32_t bytes = (uint32_t)(hi - lo) * (uint32_t)p.row_bytes;
-          const int owner = pull ? d : rank, tgt = pull ? rank : d;
-          if (pull && d != rank)
-            tile_wait(p.ag_flags[d] + d * kAgFlagStride + t, p.epoch, p.timeout_ns, p.diag, rank, 1, d, t);
-          for (int kv = 0; kv < 2; ++kv) {
-            const size_t off = ((size_t)owner * p.S_r + lo) * p.row_bytes;
-            const uint8_t* src = (!pull || d == rank) ? (kv ? ra.v_shard : ra.k_shard) + (size_t)lo * p.row_bytes
-                                                      : (kv ? p.vfull[d] : p.kfull[d]) + off;
-            uint8_t* dst = (kv ? p.vfull[tgt] : p.kfull[tgt]) + off;
-            const int n = (int)((bytes + 16383) / 16384);
-            for (int i = 0; i < n; ++i) {
-              const int bb = (g + i) & 1;
-              const uint32_t sz = min(16384u, bytes - (uint32_t)i * 16384u);
-              if (i == 0) {
-                ptx::mbar_arrive_expect_tx(&cbar[bb], sz);
-                ptx::bulk_load(cbuf + bb * 16384, src, sz, &cbar[bb]);
-              }
-              if (i + 1 < n) {
-                const uint32_t sz1 = min(16384u, bytes - (uint32_t)(i + 1) * 16384u);
-                ptx::bulk_wait_read<0>();
-                ptx::mbar_arrive_expect_tx(&cbar[bb ^ 1], sz1);
-                ptx::bulk_load(cbuf + (bb ^ 1) * 16384, src + (size_t)(i + 1) * 16384, sz1, &cbar[bb ^ 1]);
-              }
-              ptx::mbar_wait(&cbar[bb], cph[bb]);
-              cph[bb] ^= 1;
-              ptx::bulk_store(dst + (size_t)i * 16384, cbuf + bb * 16384, sz);
-              ptx::bulk_commit();
-            }
-            g += n;
-            ptx::bulk_wait<0>();
-          }
-          const bool drop = rank == p.drop_rank && t == p.drop_index && d == (pull ? rank : (rank + 1) % W);
-          if (!drop) tile_notify(pull ? p.ag_flags[rank] + d * kAgFlagStride + t : p.ag_flags[d] + rank * kAgFlagStride + t,
-                                 p.epoch);
-        }
-      }
-    }
-  } else if (warp < 8) {
-    // ============================== online softmax + epilogue (row group rg, key half hf) ==============
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
-    const int rg = warp % 4, hf = warp / 4;
-    const int row = rg * 32 + (int)lane;                    // this CTA's query row (TMEM lane)
-    const uint32_t lane_base = (uint32_t)(rg * 32) << 16;
-    const uint32_t t_o = tmem + lane_base + hf * 64;        // this warp's 64 O columns
-    const float c = p.scale_log2;
-    uint32_t g = 0, uses = 0;
-    for (int u = pair; u < n_units; u += n_pairs, ++uses) {
-      const int h = u / nqt, qt = u % nqt;
-      float m = -INFINITY, l = 0.f;
-      for (int j = 0; j < n_kv; ++j, ++g) {
-        const int b = g % 3;
-        const uint32_t t_s = tmem + lane_base + 128 + b * 128 + hf * 64;   // this warp's 64 S columns
-        const bool tr = u == pair && cip == 0 && lane == 0 && rg == 0;
-        if (tr) TL_TRACE(hf, j, 0);
-        mbar_wait_fast(&s_full[b], (g / 3) & 1);
-        ptx::tc_fence_after();
-        if (tr) TL_TRACE(hf, j, 1);
-#ifdef TL_ATTN_TRACE
-        if (p.drop_index == 12345) {   // MMA-chain-only experiment: no softmax work
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_cluster(&p_ready[b * 2 + hf], 0);
-          continue;
-        }
-#endif
-        float s[64];
-        ptx::tmem_ld32(t_s, s);
-        ptx::tmem_ld32(t_s + 32, s + 32);
-        ptx::tmem_ld_wait_fence<64>(s);
-        float mc[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) mc[i] = fmaxf(s[2 * i], s[2 * i + 1]);
-#pragma unroll
-        for (int i = 4; i < 32; ++i) mc[i & 3] = fmax3(mc[i & 3], s[2 * i], s[2 * i + 1]);
-        // row max over both key halves: exchange with the partner warp (same rows, other half)
-        float* xm = xmax + (g & 1) * 256;
-        xm[hf * 128 + row] = fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3]));
-        ptx::named_bar_sync(1 + rg, 64);
-        const float m_blk = fmaxf(xm[row], xm[128 + row]) * c;
-        if (tr) TL_TRACE(hf, j, 2);
-        // lazy max (as in the one-CTA kernel); both warps of a row take the same decision
-        const bool raise = m_blk > m + kRescaleThresh;
-        if (__any_sync(0xffffffffu, raise)) {
-          const float m_new = raise ? m_blk : m;
-          const float alpha = ptx::ex2_approx(m - m_new);
-          l *= alpha;
-          m = m_new;
-          if (j > 0) {
-            // O must hold every block < j: P(j-1).V done (o_step of buffer (g-1) % 3; s_full(g) already
-            // implies the P.V of block g-3, so that barrier is at most one phase behind)
-            mbar_wait_fast(&o_step[(g + 2) % 3], ((g - 1) / 3) & 1);
-            ptx::tc_fence_after();
-#pragma unroll 1
-            for (int k = 0; k < 2; ++k) {
-              float o[32];
-              ptx::tmem_ld32(t_o + k * 32, o);
-              ptx::tmem_ld_wait_fence<32>(o);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] *= alpha;
-              ptx::tmem_st32(t_o + k * 32, o);
-            }
-          }
-        }
-        // P = 2^(s c - m) for this warp's 64 keys, row sum, packed bf16 over the first 32 of its columns
-        const float2 cc = make_float2(c, c), mm = make_float2(-m, -m);
-        float2 acc[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float2 v = ffma2(make_float2(s[2 * i], s[2 * i + 1]), cc, mm);
-          if (kPolyMod > 0 && (i % kPolyMod) == kPolyMod - 1) {   // compile-time split (no per-element branch)
-            v = exp2_fma2(v);
-          } else {
-            v.x = ptx::ex2_approx(v.x);
-            v.y = ptx::ex2_approx(v.y);
-          }
-          acc[i & 3] = fadd2(acc[i & 3], v);
-          pk[i] = cvt_bf16x2(v.x, v.y);
-        }
-        tmem_st32u(t_s, pk);
-        acc[0] = fadd2(acc[0], acc[2]);
-        acc[1] = fadd2(acc[1], acc[3]);
-        acc[0] = fadd2(acc[0], acc[1]);
-        l += acc[0].x + acc[0].y;
-        ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (tr) TL_TRACE(hf, j, 3);
-        if (lane == 0) ptx::mbar_arrive_cluster(&p_ready[b * 2 + hf], 0);
-      }
-      // ---- epilogue: row sum over both halves, then O / l -> bf16 -> global (this warp's 64 columns)
-      xsum[hf * 128 + row] = l;
-      ptx::named_bar_sync(1 + rg, 64);
-      const float inv = 1.f / (xsum[row] + xsum[128 + row]);
-      ptx::mbar_wait(o_full, uses & 1);
-      ptx::tc_fence_after();
-      uint8_t* orow = ra.o + ((size_t)(qt * 256 + cip * 128 + row) * p.heads + h) * 256 + hf * 128;
-#pragma unroll 1
-      for (int k = 0; k < 2; ++k) {
-        float o[32];
-        ptx::tmem_ld32(t_o + k * 32, o);
-        ptx::tmem_ld_wait_fence<32>(o);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const float* w = o + 8 * v;
-          *reinterpret_cast<uint4*>(orow + k * 64 + v * 16) =
-              make_uint4(cvt_bf16x2(w[0] * inv, w[1] * inv), cvt_bf16x2(w[2] * inv, w[3] * inv),
-                         cvt_bf16x2(w[4] * inv, w[5] * inv), cvt_bf16x2(w[6] * inv, w[7] * inv));
-        }
-      }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(o_free, 0);
-      ptx::named_bar_sync(1 + rg, 64);   // xsum is rewritten by the next unit
-    }
-  }
-
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::cluster_sync();
-  if (warp == 10) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<2>(tmem, 512);
   }
 }
 
