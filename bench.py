@@ -680,6 +680,11 @@ def loopback_leg(args, M, H, I, act, oracle_rows, stream):
         loop[f"overlap_ratio_ag_{name}"] = {"comp_only_ms": round(cp, 4), "comm_only_ms": round(cm, 4),
                                             "overlap_ms": round(ov, 4),
                                             "ratio": round((cp + cm - ov) / cm, 4) if cm > 0 else None}
+        if cm > 0 and cp + cm - ov < 0:
+            loop[f"overlap_ratio_ag_{name}"]["note"] = (
+                "negative: the fused call is slower than compute-only + copy-only here, because the 8 emulated "
+                "ranks' copies (8x one rank's AG bytes) contend with the GEMMs for the one GPU's HBM and L2; "
+                "on a real TP-8 box each rank's copies go over NVLink instead")
     lc.check()
     for binding, rsb, name in ((0, 0, "sm"), (1, 0, "copy_engine"), (1, 1, "copy_engine_ag_and_rs")):
         l1, l2, lst = lb_time(binding, rsb)
