@@ -149,6 +149,9 @@ tl_status tl_comm_info(tl_comm_t comm, int* rank, int* world, int* local_ranks);
  *   "trace_events"     capacity of the device event trace (default 0 = off); see tl_trace_read
  *   "pdl"              programmatic dependent launch of the GEMM kernels (default 1): their prologue
  *                      may overlap the previous kernel in the stream (they wait before any data access)
+ *   "moe_split"        tl_moe_ag_gemm (512-wide tiles): split the last wave into 256-wide half items when it
+ *                      is at most half full, decided on the device from the routing tables (default 1).
+ *                      Speed only.
  *   "attn_poly"        tl_sp_attention: every n-th pair of exponentials is evaluated on the FMA pipe
  *                      (Cody-Waite + cubic) instead of MUFU (default 3; 0 = all on MUFU; 2,3,4,6,8).
  *                      Aligned and ragged (S/world % 128 != 0) shapes use the same split; the

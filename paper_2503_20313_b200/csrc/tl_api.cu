@@ -154,7 +154,7 @@ tl_status make_tmap_nd(CUtensorMap* m, const void* ptr, int rank, const uint64_t
 struct Options {
   int64_t comm_tile_rows = 64, channels_per_rank = 0, copy_ctas = 0, rs_order = 0, cta_pair = 2,
           raster_group = 0, num_ctas = 0, timeout_ms = 10000, debug_drop_notify = -1, debug_drop_rank = -1,
-          n_sub = 0, ag_binding = 0, ag_mode = 0, mlp_fused = 1, mlp_launches = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0;
+          n_sub = 0, ag_binding = 0, ag_mode = 0, mlp_fused = 1, mlp_launches = 0, dma_tile_rows = 0, debug_mode = 0, attn_poly = 3, debug_delay_ns = 0, trace_events = 0, pdl = 1, rs_binding = 0, rs_dma_rows = 0, moe_split = 1;
 };
 
 struct OptDesc {
@@ -181,6 +181,7 @@ const OptDesc kOpts[] = {
     {"dma_tile_rows", &Options::dma_tile_rows, 0, 1 << 20},
     {"debug_mode", &Options::debug_mode, 0, 3},
     {"attn_poly", &Options::attn_poly, 0, 8},
+    {"moe_split", &Options::moe_split, 0, 1},
     {"debug_delay_ns", &Options::debug_delay_ns, 0, 1000000},
     {"trace_events", &Options::trace_events, 0, 1ll << 28},
     {"pdl", &Options::pdl, 0, 1},
@@ -627,7 +628,9 @@ tl_status ag_gemm_impl(tl_comm* c, const void* const* A, const void* const* B, v
   p.n_blocks = (int)((N_out + bn_out - 1) / bn_out);
   p.k_blocks = (int)((K + kBK - 1) / kBK);
   set_items(p, nsub, p.ctas_per_rank / pair);
-  if (moe) p.n_full = 1 << 30;   // MoE tiles are always whole (the tile count is data dependent)
+  // MoE: the tile count is data dependent; 512-wide gather tiles split their last wave on the device
+  // (moe_split, n_full < 0), 256-wide ones are always whole
+  if (moe) p.n_full = nsub == 2 && c->opt.moe_split ? -1 : 1 << 30;
   p.tm_rows = sm.Tm;
   p.tiles_per_rank = sm.tiles_per_rank;
   p.tiles_per_channel = sm.tiles_per_channel;

@@ -89,18 +89,38 @@ __device__ __forceinline__ void tile_coords(const Params& p, int rank, int m_rot
   mb = m_perm(p, rank, m_rot, first + local % rows);
 }
 
-// Work item -> tile and the range of 256-column sub-tiles it computes.
+// Work item -> tile and the range of 256-column sub-tiles it computes (items [0, n_full) are whole tiles).
 template <int kNSub>
-__device__ __forceinline__ void item_coords(const Params& p, int item, int& t, int& sub_lo, int& sub_n) {
-  if (kNSub == 1 || item < p.n_full) {
+__device__ __forceinline__ void item_coords_n(int n_full, int item, int& t, int& sub_lo, int& sub_n) {
+  if (kNSub == 1 || item < n_full) {
     t = item;
     sub_lo = 0;
     sub_n = kNSub;
   } else {
-    const int j = item - p.n_full;
-    t = p.n_full + j / kNSub;
+    const int j = item - n_full;
+    t = n_full + j / kNSub;
     sub_lo = j % kNSub;
     sub_n = 1;
+  }
+}
+template <int kNSub>
+__device__ __forceinline__ void item_coords(const Params& p, int item, int& t, int& sub_lo, int& sub_n) {
+  item_coords_n<kNSub>(p.n_full, item, t, sub_lo, sub_n);
+}
+
+// MoE gather GroupGEMM with 512-wide tiles: the tile count comes from the device-built table, so the split
+// tail is decided here (host sets n_full < 0): when the last wave of whole tiles is at most half full, its
+// tiles run as 256-wide half items (as the dense GEMMs' split tail), e.g. MoE-4 at W = 1: 552 tiles on 74
+// pairs = 7 full waves + 34 tiles -> 68 half items instead of a half-empty eighth wave.
+__device__ __forceinline__ void moe_split(const Params& p, const RankArgs& ra, int n_pairs, int& n_full, int& total) {
+  const int T = ra.moe_tab[0] * p.n_blocks;
+  const int rem = T % n_pairs;
+  if (p.n_full < 0 && rem > 0 && 2 * rem <= n_pairs) {
+    n_full = T - rem;
+    total = T + rem;
+  } else {
+    n_full = T;
+    total = T;
   }
 }
 
@@ -295,8 +315,13 @@ __device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
   // The next kernel may be scheduled onto SMs this grid releases (its own wait keeps it ordered).
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // MoE: the number of m-tiles is data dependent (built on the device from the routing)
-  const int total = p.debug_mode == 2 ? 0 : kMoE ? ra.moe_tab[0] * p.n_blocks : p.n_items + (kFused ? p2.n_items : 0);
+  // MoE: the number of m-tiles is data dependent (built on the device from the routing); the gather
+  // flavour may split its last wave into half items (moe_split)
+  int total = p.debug_mode == 2 ? 0 : kMoE ? ra.moe_tab[0] * p.n_blocks : p.n_items + (kFused ? p2.n_items : 0);
+  int moe_nfull = 1 << 30;
+  if constexpr (kMoE == MOE_GATHER) {
+    if (p.debug_mode != 2) moe_split(p, ra, n_pairs, moe_nfull, total);
+  }
 
   // MoE producer: the 32 row gathers (tile::gather4) of every k-block are issued by two threads
   // (warp 0 lane 0: gathers 0-15 + the expert's B tile + the barrier arm; warp 2 lane 0: gathers
@@ -308,8 +333,9 @@ __device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
     const int ng = min(kGPer, 32 - g0);
     int4 ids4[kGPer];
     for (int item = pair; item < total; item += n_pairs) {
-      int mb, nb, expert;
-      moe_coords(p, ra, item, mb, nb, expert);
+      int mb, nb, expert, t, sub_lo, sub_n;
+      item_coords_n<kNSub>(moe_nfull, item, t, sub_lo, sub_n);
+      moe_coords(p, ra, t, mb, nb, expert);
       const int row0 = mb * BM + cta_in_pair * 128;
       // dynamic mapping: this tile's rows are tokens [tok_lo, tok_hi] (sorted), gathered by id
       const int* tb = ra.moe_tab + 4 + 3 * mb;
@@ -340,8 +366,7 @@ __device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
             ptx::tma_gather4_elect<kPair>(&ra.tm_a, &full[stage], sa + (g0 + i) * 512, kc, ids4[i].x, ids4[i].y,
                                           ids4[i].z, ids4[i].w);
         if (is_main && lane == 0) {
-#pragma unroll
-          for (int sub = 0; sub < kNSub; ++sub) {   // one gathered A stage feeds kNSub 256-wide sub-tiles
+          for (int sub = sub_lo; sub < sub_lo + sub_n; ++sub) {   // one gathered A stage feeds kNSub sub-tiles
             uint8_t* sbs = sb + sub * L::kBBox;
             if constexpr (kEpi == EPI_SILU_MUL || kEpi == EPI_GELU_MUL) {
               const int nrow = nb * 128 * kNSub + sub * 128;
@@ -357,7 +382,7 @@ __device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
             }
           }
           if (cta_in_pair == 0)
-            ptx::mbar_arrive_expect_tx(&full[stage], (kAStage + kNSub * L::kBBox) * kPair);
+            ptx::mbar_arrive_expect_tx(&full[stage], (kAStage + sub_n * L::kBBox) * kPair);
           else
             ptx::mbar_arrive_cluster(&full[stage], 0);
         }
@@ -469,7 +494,7 @@ __device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
         const Params& p = ph2 ? p2 : p1;
         const int itl = ph2 ? item - p1.n_items : item;
         int t, sub_lo, sub_n;
-        item_coords<kNSub>(p, itl, t, sub_lo, sub_n);
+        item_coords_n<kNSub>(kMoE == MOE_GATHER ? moe_nfull : p.n_full, itl, t, sub_lo, sub_n);
         if constexpr (kNSub == 2 && kMoE == MOE_NONE) {
           const int epi = ph2 ? phase2_epi(p) : kEpi;
           if (epi != EPI_RS) {
@@ -577,9 +602,9 @@ __device__ __forceinline__ void gemm_body(const Params& p1, const Params& p2) {
       const int itl = ph2 ? item - p1.n_items : item;
       const int epi = ph2 ? phase2_epi(p) : kEpi;
       int t, sub_lo, sub_n, mb, nb, expert;
-      item_coords<kNSub>(p, itl, t, sub_lo, sub_n);
+      item_coords_n<kNSub>(kMoE == MOE_GATHER ? moe_nfull : p.n_full, itl, t, sub_lo, sub_n);
       if constexpr (kMoE == MOE_SCATTER) mb = moe_scatter_tile(p, ra, item, nb);
-      else if constexpr (kMoE) moe_coords(p, ra, item, mb, nb, expert);
+      else if constexpr (kMoE) moe_coords(p, ra, t, mb, nb, expert);
       else tile_coords(p, rank, ra.m_rot, t, mb, nb);
       clamp_subs<kNSub, kMoE>(p, nb, sub_lo, sub_n, epi);
       (void)expert;

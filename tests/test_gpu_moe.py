@@ -206,3 +206,31 @@ def test_moe_layer_bench_config_w1_sampled(tl):
     ref = BW._moe_oracle_tokens(X, ids, wts, f(W1s), f(W2s), toks)
     got = out[torch.as_tensor(toks, device="cuda")].float().cpu().double().numpy()
     assert_parity(got, ref)
+
+
+@pytest.mark.parametrize("M,H,N_out,E,topk", [(8192, 4096, 2048, 8, 2), (2048, 512, 512, 4, 2), (1024, 256, 384, 3, 1)])
+def test_moe_split_tail_bitwise(tl, M, H, N_out, E, topk):
+    """Option moe_split (default on): the gather GroupGEMM's last wave of 512-wide tiles runs as 256-wide
+    half items when it is at most half full (decided on the device from the routing tables; MoE-4 at W = 1:
+    552 tiles on 74 pairs).  Tiles are computed the same way, so the output is bitwise identical to whole
+    tiles; also with CTA counts that put the split on other remainders."""
+    X = TI._randn((M, H), 3, 0).cuda()
+    W1 = TI.moe_weights(E, 2 * N_out, H, 1, seed=4)[0].cuda()
+    ids = TI.moe_routing(M, E, topk, seed=5).cuda()
+    outs = []
+    for split, ctas in ((0, 0), (1, 0), (1, 100), (1, 60)):
+        c = tl.Comm.single(0, max_M=M, max_H=H)
+        c.set_option("moe_split", split)
+        c.set_option("num_ctas", ctas)
+        R = tl.moe_capacity(c, M, topk, E)
+        Y = torch.empty(R, N_out, device="cuda", dtype=torch.bfloat16)
+        rows = torch.empty(R, device="cuda", dtype=torch.int32)
+        offs = torch.empty(E + 1, device="cuda", dtype=torch.int32)
+        tl.moe_ag_gemm(c, X, ids, W1, Y, rows, offs, act=tl.ACT_SILU_MUL)
+        torch.cuda.synchronize()
+        assert c.check()[0] == 0
+        n = int(offs[-1].item())
+        outs.append((Y[:n].clone(), rows[:n].clone()))
+        c.close()
+    for Y, rows in outs[1:]:
+        assert torch.equal(rows, outs[0][1]) and torch.equal(Y, outs[0][0])
