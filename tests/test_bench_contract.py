@@ -35,7 +35,7 @@ def test_reference_arm_json(workload):
         assert d["config"] == BW.attn_config(1)
 
 
-@pytest.mark.parametrize("gpus", [2])
+@pytest.mark.parametrize("gpus", [2, 4])
 def test_self_launch_dry_run(gpus):
     """`bench.py --gpus N` outside torchrun re-executes itself with N ranks (gloo in --dry-run): exactly one
     JSON line, from rank 0, for the W = N workload, with the max over ranks taken across all N."""
