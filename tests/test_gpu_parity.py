@@ -412,6 +412,8 @@ def test_ag_dma_dropped_notify_times_out(tl):
     ("llama7b", 8192, 4096, 11008, 8, 3),     # BASELINE configs[1] (8 ranks, loopback): rank 3's whole block
     ("llama70b", 8192, 8192, 28672, 2, None),  # configs[2] at W=2
     ("mixtral", 16384, 4096, 14336, 4, None),  # configs[3] at W=4
+    ("llama7b_M32768", 32768, 4096, 11008, 1, None),  # configs[4] M sweep, largest M
+    ("llama7b_M1024", 1024, 4096, 11008, 8, 5),       # configs[4] M sweep, smallest M at 8 ranks (128 rows/rank)
 ])
 def test_full_size_sampled_rows(tl, name, M, H, I, W, block):
     """Full BASELINE.json sizes; the oracle is evaluated exactly on sampled rows (rows are
