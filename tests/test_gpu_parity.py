@@ -631,3 +631,31 @@ def test_parity_check_rejects_a_corrupted_gpu_tile(tl):
     bad[640:768, 512:768] *= 1.01
     rep = parity_report(bad, ref)
     assert not rep["ok"] and rep["worst_tile"] == (640, 512) and rep["global"] < TOL
+
+
+@pytest.mark.parametrize("act", [TI.ACT_NONE, TI.ACT_GELU_TANH_MUL])
+@pytest.mark.parametrize("W", [1, 8])
+def test_full_size_other_activations(tl, act, W):
+    """The LLaMA-7B layer (M = 8192) with the two other activations of R1/R2 (identity: GEMM1 is I/W wide;
+    GeLU(tanh)*up), at W = 1 and over 8 loopback ranks: sampled rows of every rank's block plus the first
+    128-row tile, element-wise against the fp64 oracle."""
+    M, H, I = 8192, 4096, 11008
+    X, G, U, W2 = TI.mlp_full(M, H, I, seed=1)
+    Xs, W1s, W2s = TI.shard_mlp(X, G, U, W2, W, act)
+    del X, G, U, W2
+    Mr = M // W
+    outs = [empty(Mr, H) for _ in range(W)]
+    if W == 1:
+        c = tl.Comm.single(0, max_M=M, max_H=H)
+        c.mlp_forward(cuda(Xs[0]), cuda(W1s[0]), cuda(W2s[0]), outs[0], act=act)
+        torch.cuda.synchronize()
+    else:
+        c = tl.Comm.loopback(W, 0, max_M=M, max_H=H)
+        c.mlp_forward_lb([cuda(x) for x in Xs], [cuda(w) for w in W1s], [cuda(w) for w in W2s], outs, act=act)
+    assert c.check()[0] == 0
+    rows = sorted({r * Mr + o for r in range(W) for o in (0, 7, Mr // 2, Mr - 1)} | set(range(128)))
+    ref = O.mlp_forward_rows([TI.to_f64(t) for t in Xs], [TI.to_f64(t) for t in W1s], [TI.to_f64(t) for t in W2s],
+                             act, rows)
+    full = torch.cat(outs).float().cpu().double().numpy()
+    assert_parity(full[rows], np.stack([ref[i] for i in rows]))
+    del c
