@@ -291,3 +291,41 @@ def test_attention_copy_engine_dropped_notify_times_out(tl):
     tl.sp_attention_lb(comm, qd, kd, vd, outs)
     st, diag = comm.check()
     assert st != 0 and diag[1] == 1
+
+
+def test_attention_paper_shape_attn2_32k_sampled(tl):
+    """Attn-2 (64 heads, d 128) at S = 32k over 4 ranks: sampled query rows of every rank against
+    the oracle evaluated row by row over the whole gathered K/V."""
+    W, S, heads, D = 4, 32768, 64, 128
+    Qs, Ks, Vs = TI.attention_inputs(S, heads, D, W, seed=6)
+    comm = _comm(tl, W, S, heads)
+    qd, kd, vd = ([t.cuda() for t in L] for L in (Qs, Ks, Vs))
+    outs = [torch.empty_like(q) for q in qd]
+    tl.sp_attention_lb(comm, qd, kd, vd, outs)
+    st, diag = comm.check()
+    assert st == 0, diag
+    rng = np.random.default_rng(1)
+    K64, V64 = (np.concatenate([TI.to_f64(t) for t in L], 0) for L in (Ks, Vs))
+    for r in range(W):
+        rows = rng.choice(S // W, 3, replace=False)
+        ref = O.sp_attention([TI.to_f64(Qs[r])[rows]], [K64], [V64], D ** -0.5)[0]
+        got = outs[r][torch.as_tensor(rows, device="cuda")].float().cpu().double().numpy()
+        assert_parity(got, ref)
+
+
+def test_attention_longest_sequence_sampled(tl):
+    """The paper's longest sequence (S = 128k) on one GPU with 4 heads: 1024 KV blocks per
+    query tile, so the online softmax (lazy max, fp32 O and row sums) runs its longest accumulation;
+    sampled rows against the oracle."""
+    S, heads, D = 131072, 4, 128
+    Qs, Ks, Vs = TI.attention_inputs(S, heads, D, 1, seed=7)
+    comm = tl.Comm.single(0, max_M=128, max_H=128)
+    q, k, v = Qs[0].cuda(), Ks[0].cuda(), Vs[0].cuda()
+    o = torch.empty_like(q)
+    tl.sp_attention(comm, q, k, v, o)
+    st, diag = comm.check()
+    assert st == 0, diag
+    rows = np.sort(np.random.default_rng(2).choice(S, 12, replace=False))
+    ref = O.sp_attention([TI.to_f64(Qs[0])[rows]], [TI.to_f64(Ks[0])], [TI.to_f64(Vs[0])], D ** -0.5)[0]
+    got = o[torch.as_tensor(rows, device="cuda")].float().cpu().double().numpy()
+    assert_parity(got, ref)
